@@ -1,0 +1,51 @@
+// Argument blocks shared by the host launcher (lgp_*.cpp, compiled by nvcc/g++)
+// and the NVRTC-generated kernels (this text is prepended to every JIT source).
+// Plain C layout only: both sides must agree byte for byte.
+#ifndef LGP_JIT_ABI_H_
+#define LGP_JIT_ABI_H_
+
+#define LGP_MAX_KC 48
+#define LGP_MAX_PC 48
+
+// Per-point feature preparation: x (FP64, n x d) -> row / column features (FP32).
+struct LgpPrepArgs {
+  const double* x;      // points, n x d row-major
+  const double* ctr;    // d centring offsets (column mean of the column set)
+  float* fr;            // [n_pad][FR] row-side features (may be null)
+  float* fc;            // [n_pad][FC] column-side features (may be null)
+  long long row0;       // first point to prepare (sharded row slice)
+  long long n;          // points in this slice
+  long long n_pad;      // padded slice length (zero features beyond n)
+  double pc[LGP_MAX_PC];
+};
+
+// Fused matrix-free K·V: one CTA = (row block, column segment, RHS pass).
+struct LgpMatvecArgs {
+  const float* fr;      // [n_rows_pad][FR]
+  const float* fc;      // [n_cols_pad][FC]
+  const double* v;      // packed RHS [n_pass][n_cols_pad][TB]
+  double* partial;      // [n_seg][n_pass][n_rows_pad][TB]
+  const int* done;      // optional early-exit flag (solver loops), may be null
+  int n_rows_pad;
+  int n_cols_pad;
+  int n_rb;             // row blocks
+  int n_seg;            // column segments
+  int n_pass;           // RHS passes of TB columns
+  int tiles_per_seg;
+  int n_tiles;          // column tiles in total
+  int pad_;
+  float kc[LGP_MAX_KC];
+};
+
+// Dense FP64 cross-covariance / diagonal.
+struct LgpGramArgs {
+  const double* x;      // rows, n_rows x d
+  const double* y;      // cols, n_cols x d
+  double* out;          // n_rows x ld
+  long long n_rows;
+  long long n_cols;
+  long long ld;
+  double pc[LGP_MAX_PC];
+};
+
+#endif  // LGP_JIT_ABI_H_

@@ -1,0 +1,315 @@
+// Matvec engine (feature prep -> fused K1 -> FP64 epilogue) and the
+// device-resident CG / Lanczos drivers.
+//
+// Multi-GPU (world > 1): rank g owns rows [g*S, min((g+1)*S, n)) of K with
+// S = ceil(n/world); X is replicated. Each iteration computes the local rows
+// of the product, all-gathers the slices in place (one NCCL call over
+// NVLink), and then runs the FP64 vector updates redundantly on the full
+// vectors. All ranks hold bit-identical state, the host loop's stop decision
+// is identical on every rank, and no scalar all-reduce is needed.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "lgp_internal.h"
+
+namespace lgp {
+
+void Context::activate() { LGP_CUDA_CHECK(cudaSetDevice(device)); }
+
+void* Context::scratch_get(const std::string& name, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  DeviceBuffer& b = scratch[name];
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      LGP_CUDA_CHECK(cudaStreamSynchronize(stream));
+      LGP_CUDA_CHECK(cudaFree(b.ptr));
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    const size_t want = bytes + bytes / 8;  // growth slack
+    LGP_CUDA_CHECK(cudaMalloc(&b.ptr, want));
+    b.bytes = want;
+  }
+  return b.ptr;
+}
+
+namespace {
+int pick_tb(int t) {
+  if (t >= 16) return 16;
+  int tb = 1;
+  while (tb < t) tb <<= 1;
+  return tb;
+}
+template <class T>
+T ceil_div(T a, T b) {
+  return (a + b - 1) / b;
+}
+void launch(Context* ctx, CUfunction f, unsigned gx, unsigned gy, unsigned bx, size_t smem,
+            void* args) {
+  void* params[] = {args};
+  LGP_CU_CHECK(drv::LaunchKernel(f, gx, gy, 1, bx, 1, 1, (unsigned)smem, (CUstream)ctx->stream,
+                              params, nullptr));
+  ++ctx->launches;
+}
+}  // namespace
+
+void MatvecOp::prepare() {
+  const int tb = pick_tb(t);
+  plan = make_plan(k->tree, rows->d, tb, flags);
+  mod = get_module(ctx, plan);
+  const Tuning& tu = plan.tune;
+  const int rows_per_cta = tu.threads * tu.r;
+  n_rb = (int)ceil_div<int64_t>(std::max<int64_t>(n_rows, 1), rows_per_cta);
+  n_rows_pad = n_rb * rows_per_cta;
+  n_tiles = (int)ceil_div<int64_t>(std::max<int64_t>(cols->n, 1), tu.cc);
+  n_cols_pad = n_tiles * tu.cc;
+  n_pass = ceil_div(t, tb);
+
+  // Column split so that (row blocks x segments x passes) CTAs fill whole
+  // waves of resident CTAs: minimise waves / segments (+ partial traffic).
+  const int slots = ctx->sm_count * mod->blocks_per_sm;
+  const int64_t base = (int64_t)n_rb * n_pass;
+  int best = 1;
+  double best_cost = 1e30;
+  for (int s = 1; s <= std::min(n_tiles, 64); ++s) {
+    const int64_t items = base * s;
+    const double waves = (double)ceil_div<int64_t>(items, slots);
+    const double cost = waves / s + 0.002 * s;
+    if (cost < best_cost - 1e-12) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  tiles_per_seg = ceil_div(n_tiles, best);
+  n_seg = ceil_div(n_tiles, tiles_per_seg);
+
+  fr = (float*)ctx->scratch_get(tag + ".fr", (size_t)n_rows_pad * plan.fr * 4);
+  fc = (float*)ctx->scratch_get(tag + ".fc", (size_t)n_cols_pad * plan.fc * 4);
+  vpack = (double*)ctx->scratch_get(tag + ".v", (size_t)n_pass * n_cols_pad * tb * 8);
+  partial = (double*)ctx->scratch_get(tag + ".part", (size_t)n_seg * n_pass * n_rows_pad * tb * 8);
+
+  // features of the local rows and of all columns, centred on the column set
+  LgpPrepArgs pa = plan.prep;
+  pa.x = rows->x;
+  pa.ctr = cols->ctr;
+  pa.fr = fr;
+  pa.fc = nullptr;
+  pa.row0 = row0;
+  pa.n = n_rows;
+  pa.n_pad = n_rows_pad;
+  launch(ctx, mod->prep, (unsigned)ceil_div<int64_t>(n_rows_pad, 128), 1, 128, 0, &pa);
+  LgpPrepArgs pc = plan.prep;
+  pc.x = cols->x;
+  pc.ctr = cols->ctr;
+  pc.fr = nullptr;
+  pc.fc = fc;
+  pc.row0 = 0;
+  pc.n = cols->n;
+  pc.n_pad = n_cols_pad;
+  launch(ctx, mod->prep, (unsigned)ceil_div<int64_t>(n_cols_pad, 128), 1, 128, 0, &pc);
+}
+
+void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const double* noise_v,
+                   const int* done) {
+  const int tb = plan.tune.tb;
+  vec::pack_rhs(ctx, V_dev, cols->n, t, n_cols_pad, tb, n_pass, vpack, done);
+  LgpMatvecArgs a = plan.mv;
+  a.fr = fr;
+  a.fc = fc;
+  a.v = vpack;
+  a.partial = partial;
+  a.done = done;
+  a.n_rows_pad = n_rows_pad;
+  a.n_cols_pad = n_cols_pad;
+  a.n_rb = n_rb;
+  a.n_seg = n_seg;
+  a.n_pass = n_pass;
+  a.tiles_per_seg = tiles_per_seg;
+  a.n_tiles = n_tiles;
+  const int64_t grid = (int64_t)n_rb * n_seg * n_pass;
+  if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
+  launch(ctx, mod->matvec, (unsigned)grid, 1, plan.tune.threads, plan.smem_bytes, &a);
+  vec::epilogue(ctx, partial, n_seg, n_pass, n_rows_pad, tb, n_rows, t, plan.root_scale, noise,
+                noise_v, out_dev, done);
+}
+
+// ------------------------------------------------------------------ CG
+struct CgBuffers {
+  double *x, *r, *p, *ap, *part, *bb;
+  vec::CgState s;
+};
+
+static CgBuffers cg_buffers(Context* ctx, int64_t n_alloc, int t, int nblk) {
+  CgBuffers b;
+  const size_t vb = (size_t)n_alloc * t * 8;
+  b.x = (double*)ctx->scratch_get("cg.x", vb);
+  b.r = (double*)ctx->scratch_get("cg.r", vb);
+  b.p = (double*)ctx->scratch_get("cg.p", vb);
+  b.ap = (double*)ctx->scratch_get("cg.ap", vb);
+  b.part = (double*)ctx->scratch_get("cg.part", (size_t)nblk * t * 8);
+  char* sc = (char*)ctx->scratch_get("cg.scal", (size_t)t * 8 * 8 + 64);
+  double* d = (double*)sc;
+  b.bb = d;
+  b.s.rs = d + t;
+  b.s.tol = d + 2 * t;
+  b.s.step = d + 3 * t;
+  b.s.beta = d + 4 * t;
+  b.s.res = d + 5 * t;
+  int* iv = (int*)(d + 6 * t);
+  b.s.active = iv;
+  b.s.iters = iv + t;
+  b.s.status = iv + 2 * t;
+  b.s.done = iv + 2 * t + 1;
+  b.s.bad_col = iv + 2 * t + 2;
+  return b;
+}
+
+// B_dev: n_alloc x t device buffer (rows >= n ignored). Results stay on the
+// device in the returned buffers' x; iterations / residuals copied to host.
+void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double noise,
+               const double* B_dev, int t, double rel_tol, int max_iter, double** x_dev,
+               int32_t* iters_out, double* res_out) {
+  const int64_t n = pts->n;
+  int64_t r0 = 0, r1 = n;
+  lgp_partition(n, ctx->world, ctx->rank, &r0, &r1);
+  const int64_t S = ceil_div<int64_t>(n, ctx->world);
+  const int64_t n_alloc = S * ctx->world;
+  const int nblk = vec::reduce_blocks(n, t);
+  CgBuffers b = cg_buffers(ctx, n_alloc, t, nblk);
+  if (max_iter <= 0) max_iter = (int)std::min<int64_t>(n, 1000);
+
+  MatvecOp op;
+  op.ctx = ctx;
+  op.k = k;
+  op.rows = pts;
+  op.cols = pts;
+  op.row0 = r0;
+  op.n_rows = r1 - r0;
+  op.t = t;
+  op.tag = "cg.mv";
+  op.prepare();
+
+  vec::dot_partial(ctx, B_dev, B_dev, n, t, b.part, nullptr);
+  vec::dot_final(ctx, b.part, nblk, t, b.bb, nullptr);
+  vec::cg_init(ctx, B_dev, b.x, b.r, b.p, n, t, rel_tol, b.bb, b.s);
+
+  // host-side stop checks: every iteration for large operators, else in
+  // batches (kernels after convergence early-exit on the device flag)
+  const double entries = (double)n * (double)n * t;
+  const int check_every = entries > 2e8 ? 1 : 8;
+  int done_h = 0;
+  LGP_CUDA_CHECK(cudaMemcpyAsync(&done_h, b.s.done, sizeof(int), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  for (int it = 1; it <= max_iter && !done_h; ++it) {
+    op.run(b.p, b.ap + r0 * t, noise, b.p + r0 * t, b.s.done);
+    if (ctx->world > 1) comm_allgather_inplace(ctx->comm, b.ap, (size_t)S * t, ctx->stream);
+    vec::dot_partial(ctx, b.p, b.ap, n, t, b.part, b.s.done);
+    vec::cg_fin_pap(ctx, b.part, nblk, t, b.s);
+    vec::cg_update_xr(ctx, b.x, b.r, b.p, b.ap, n, t, b.s, b.part);
+    vec::cg_fin_rs(ctx, b.part, nblk, t, it, max_iter, b.s);
+    vec::cg_update_p(ctx, b.p, b.r, n, t, b.s);
+    if (it % check_every == 0 || it == max_iter) {
+      LGP_CUDA_CHECK(cudaMemcpyAsync(&done_h, b.s.done, sizeof(int), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+      LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  int status[2] = {0, -1};
+  LGP_CUDA_CHECK(cudaMemcpyAsync(status, b.s.status, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  LGP_CUDA_CHECK(cudaMemcpyAsync(iters_out, b.s.iters, t * sizeof(int), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  LGP_CUDA_CHECK(cudaMemcpyAsync(res_out, b.s.res, t * sizeof(double), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  if (status[0] != 0)
+    throw Error(LGP_E_NOT_SPD, "CG breakdown: p.A.p is not positive (column " +
+                                   std::to_string(status[1]) + ")");
+  *x_dev = b.x;
+}
+
+// ------------------------------------------------------------- Lanczos
+void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, double noise,
+                    const double* Z_dev, int t, int steps, double* alphas, double* betas,
+                    int32_t* steps_out) {
+  const int64_t n = pts->n;
+  int64_t r0 = 0, r1 = n;
+  lgp_partition(n, ctx->world, ctx->rank, &r0, &r1);
+  const int64_t S = ceil_div<int64_t>(n, ctx->world);
+  const int64_t n_alloc = S * ctx->world;
+  const int nblk = vec::reduce_blocks(n, t);
+  const size_t vb = (size_t)n_alloc * t;
+  double* basis = (double*)ctx->scratch_get("lz.basis", vb * steps * 8);
+  double* w = (double*)ctx->scratch_get("lz.w", vb * 8);
+  double* part = (double*)ctx->scratch_get("lz.part", (size_t)nblk * steps * t * 8);
+  char* sc = (char*)ctx->scratch_get("lz.scal", (size_t)t * 8 * (2 * steps + steps + 4) + 64);
+  double* d = (double*)sc;
+  vec::LzState s;
+  s.alpha = d;
+  s.beta = d + (size_t)t * steps;
+  s.h = d + (size_t)2 * t * steps;
+  s.a_cur = s.h + (size_t)t * steps;
+  s.nrm = s.a_cur + t;
+  double* zz = s.nrm + t;
+  int* iv = (int*)(zz + t);
+  s.active = iv;
+  s.count = iv + t;
+  s.done = iv + 2 * t;
+  LGP_CUDA_CHECK(cudaMemsetAsync(s.alpha, 0, (size_t)2 * t * steps * 8, ctx->stream));
+
+  MatvecOp op;
+  op.ctx = ctx;
+  op.k = k;
+  op.rows = pts;
+  op.cols = pts;
+  op.row0 = r0;
+  op.n_rows = r1 - r0;
+  op.t = t;
+  op.tag = "lz.mv";
+  op.prepare();
+
+  vec::dot_partial(ctx, Z_dev, Z_dev, n, t, part, nullptr);
+  vec::dot_final(ctx, part, nblk, t, zz, nullptr);
+  vec::lz_init(ctx, Z_dev, basis, n, t, zz, s);
+  const int64_t stride = (int64_t)n_alloc * t;
+  const double entries = (double)n * (double)n * t;
+  const int check_every = entries > 2e8 ? 1 : 8;
+  int done_h = 0;
+  for (int j = 0; j < steps && !done_h; ++j) {
+    double* q = basis + (size_t)j * stride;
+    const double* qprev = j > 0 ? basis + (size_t)(j - 1) * stride : nullptr;
+    op.run(q, w + r0 * t, noise, q + r0 * t, s.done);
+    if (ctx->world > 1) comm_allgather_inplace(ctx->comm, w, (size_t)S * t, ctx->stream);
+    vec::dot_partial(ctx, q, w, n, t, part, s.done);
+    vec::lz_fin_alpha(ctx, part, nblk, t, j, steps, s);
+    vec::lz_update1(ctx, w, q, qprev, n, t, j, steps, s);
+    if (j == steps - 1) break;  // the last step needs no beta (solvers.py:148-149)
+    vec::lz_multidot(ctx, basis, stride, j + 1, w, n, t, part, s.done);
+    vec::lz_fin_h(ctx, part, nblk, j + 1, t, s);
+    vec::lz_update2(ctx, w, basis, stride, j + 1, n, t, s, part);
+    vec::lz_fin_beta(ctx, part, nblk, t, j, steps, s);
+    vec::lz_normalize(ctx, w, basis + (size_t)(j + 1) * stride, n, t, s);
+    if ((j + 1) % check_every == 0) {
+      LGP_CUDA_CHECK(cudaMemcpyAsync(&done_h, s.done, sizeof(int), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+      LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  std::vector<double> al((size_t)t * steps), be((size_t)t * steps);
+  LGP_CUDA_CHECK(cudaMemcpyAsync(al.data(), s.alpha, al.size() * 8, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  LGP_CUDA_CHECK(cudaMemcpyAsync(be.data(), s.beta, be.size() * 8, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  LGP_CUDA_CHECK(cudaMemcpyAsync(steps_out, s.count, t * sizeof(int), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  for (int c = 0; c < t; ++c) {
+    for (int j = 0; j < steps; ++j) alphas[(size_t)c * steps + j] = al[(size_t)c * steps + j];
+    for (int j = 0; j + 1 < steps; ++j)
+      betas[(size_t)c * (steps - 1) + j] = be[(size_t)c * steps + j];
+  }
+}
+
+}  // namespace lgp

@@ -1,0 +1,263 @@
+// Internal declarations shared by the C-ABI front end, the kernel-tree code
+// generator / NVRTC JIT, the AOT FP64 vector kernels and the solver drivers.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lightgp.h"
+#include "jit/lgp_jit_abi.h"
+
+namespace lgp {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+// driver API, resolved lazily (lgp_driver.cpp)
+namespace drv {
+CUresult ModuleLoadData(CUmodule* m, const void* image);
+CUresult ModuleUnload(CUmodule m);
+CUresult ModuleGetFunction(CUfunction* f, CUmodule m, const char* name);
+CUresult FuncSetAttribute(CUfunction f, CUfunction_attribute a, int v);
+CUresult FuncGetAttribute(int* v, CUfunction_attribute a, CUfunction f);
+CUresult OccupancyMaxActiveBlocksPerMultiprocessor(int* n, CUfunction f, int bs, size_t smem);
+CUresult LaunchKernel(CUfunction f, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
+                      unsigned by, unsigned bz, unsigned smem, CUstream s, void** params,
+                      void** extra);
+CUresult GetErrorString(CUresult r, const char** s);
+}  // namespace drv
+
+#define LGP_CUDA_CHECK(expr)                                                              \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      throw ::lgp::Error(_e == cudaErrorMemoryAllocation ? LGP_E_OOM : LGP_E_CUDA,        \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+  } while (0)
+
+#define LGP_CU_CHECK(expr)                                                                \
+  do {                                                                                    \
+    CUresult _r = (expr);                                                                 \
+    if (_r != CUDA_SUCCESS) {                                                             \
+      const char* _s = nullptr;                                                           \
+      ::lgp::drv::GetErrorString(_r, &_s);                                                          \
+      throw ::lgp::Error(_r == CUDA_ERROR_OUT_OF_MEMORY ? LGP_E_OOM : LGP_E_CUDA,        \
+                         std::string(#expr) + ": " + (_s ? _s : "?"));                   \
+    }                                                                                     \
+  } while (0)
+
+// ---------------------------------------------------------- kernel trees
+struct Node {
+  int kind;
+  double p[2];
+};
+
+struct Tree {
+  std::vector<Node> nodes;  // pre-order
+  bool has_linear() const;
+};
+
+int node_arity(int kind);
+int node_nparams(int kind);
+
+// Tuning of one matvec module (compile-time constants of the JIT kernel).
+struct Tuning {
+  int tb = 1;        // RHS per pass
+  int r = 8;         // rows per thread
+  int threads = 256; // CTA size
+  int cc = 64;       // columns per shared-memory tile
+  int stages = 4;    // TMA pipeline depth
+  int minb = 1;      // __launch_bounds__ min blocks
+};
+
+// Output of the code generator for (tree structure, D, TB, flags).
+struct Plan {
+  std::string key;          // cache key = full source text + options
+  std::string source;       // NVRTC source
+  Tuning tune;
+  int d = 0, fr = 0, fc = 0;
+  bool signed_vals = false;
+  double root_scale = 1.0;  // product of Scale nodes on the root chain (FP64 epilogue)
+  LgpPrepArgs prep{};       // pc[] filled
+  LgpMatvecArgs mv{};       // kc[] filled
+  LgpGramArgs gram{};       // pc[] filled (includes the root scale)
+  size_t smem_bytes = 0;
+};
+
+Plan make_plan(const Tree& tree, int d, int tb, uint32_t flags);
+
+// A loaded JIT module.
+struct Module {
+  CUmodule mod = nullptr;
+  CUfunction prep = nullptr, matvec = nullptr, gram = nullptr, diag = nullptr;
+  int blocks_per_sm = 1;
+  int regs = 0;
+  std::string log;
+};
+
+// Compile (or fetch from the in-memory / on-disk cache) the module for a plan.
+Module* get_module(struct Context* ctx, const Plan& plan);
+
+// ------------------------------------------------------------- contexts
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct Comm;  // NCCL communicator (dlopen'ed), null for world == 1
+
+struct Context {
+  int device = 0;
+  int rank = 0;
+  int world = 1;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  Comm* comm = nullptr;
+  std::recursive_mutex mu;
+  std::map<std::string, std::unique_ptr<Module>> modules;
+  std::map<std::string, DeviceBuffer> scratch;
+  uint64_t launches = 0;
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
+
+  void* scratch_get(const std::string& name, size_t bytes);  // grow-only
+  void activate();  // cudaSetDevice for the calling thread
+};
+
+struct KernelHandle {
+  Context* ctx;
+  Tree tree;
+};
+
+struct Points {
+  Context* ctx;
+  int64_t n = 0;
+  int32_t d = 0;
+  double* x = nullptr;        // device n x d FP64
+  double* ctr = nullptr;      // device d FP64: column mean (centring of features)
+  std::vector<double> center; // host copy of ctr
+};
+
+// ------------------------------------------------------ communicator
+Comm* comm_create(int rank, int world, const uint8_t* id128, cudaStream_t stream);
+void comm_destroy(Comm* c);
+void comm_unique_id(uint8_t* out128);
+// in-place all-gather: buf holds world slices of `count` doubles; this
+// rank's slice is at buf + rank*count.
+void comm_allgather_inplace(Comm* c, double* buf, size_t count, cudaStream_t stream);
+
+// ------------------------------------------------------ matvec engine
+// Device-resident matvec: out_rows[n_rows_local x t] for rows
+// [row0, row0+n_rows_local) of `rows` against all of `cols`.
+// V_dev: n_cols x t (device). out_dev: n_rows_local x t (device).
+// noise_v: if non-null, rows-aligned V used for the + noise·V term.
+struct MatvecOp {
+  Context* ctx;
+  const KernelHandle* k;
+  const Points* rows;
+  const Points* cols;
+  int64_t row0 = 0, n_rows = 0;  // local row slice
+  int t = 1;
+  uint32_t flags = 0;
+  // prepared state
+  Plan plan;
+  Module* mod = nullptr;
+  float* fr = nullptr;
+  float* fc = nullptr;
+  double* vpack = nullptr;
+  double* partial = nullptr;
+  int n_rows_pad = 0, n_cols_pad = 0, n_rb = 0, n_seg = 0, n_pass = 0, n_tiles = 0,
+      tiles_per_seg = 0;
+  std::string tag;
+
+  void prepare();  // features, scratch, schedule
+  void run(const double* V_dev, double* out_dev, double noise, const double* noise_v,
+           const int* done);
+};
+
+// ------------------------------------------------------ solver drivers
+void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double noise,
+               const double* B_dev, int t, double rel_tol, int max_iter, double** x_dev,
+               int32_t* iters_out, double* res_out);
+void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, double noise,
+                    const double* Z_dev, int t, int steps, double* alphas, double* betas,
+                    int32_t* steps_out);
+std::string jit_compile(const std::string& source, std::string* log_out);
+
+// ------------------------------------------------------ AOT FP64 kernels
+namespace vec {
+int reduce_blocks(int64_t n, int t);
+void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int tb, int n_pass,
+              double* out, const int* done);
+void epilogue(Context* c, const double* partial, int n_seg, int n_pass, int64_t rows_pad, int tb,
+              int64_t n_rows, int t, double scale, double noise, const double* noise_v,
+              double* out, const int* done);
+// column dots: part[blk][t] then final[t] (deterministic order)
+void dot_partial(Context* c, const double* a, const double* b, int64_t n, int t, double* part,
+                 const int* done);
+void dot_final(Context* c, const double* part, int nblk, int t, double* out, const int* done);
+void fill(Context* c, double* p, int64_t n, double v);
+
+// CG (solvers.py:87-123), see lgp_vec.cu
+struct CgState {
+  double* rs;      // [t]
+  double* tol;     // [t]
+  double* step;    // [t]
+  double* beta;    // [t]
+  double* res;     // [t]
+  int* active;     // [t]
+  int* iters;      // [t]
+  int* status;     // [1]: 0 ok, 1 breakdown
+  int* done;       // [1]
+  int* bad_col;    // [1]
+};
+void cg_init(Context* c, const double* b, double* x, double* r, double* p, int64_t n, int t,
+             double rel_tol, const double* bb_final, CgState s);
+void cg_fin_pap(Context* c, const double* part, int nblk, int t, CgState s);
+void cg_update_xr(Context* c, double* x, double* r, const double* p, const double* ap, int64_t n,
+                  int t, CgState s, double* part);
+void cg_fin_rs(Context* c, const double* part, int nblk, int t, int it, int max_iter, CgState s);
+void cg_update_p(Context* c, double* p, const double* r, int64_t n, int t, CgState s);
+
+// Lanczos (solvers.py:126-154), see lgp_vec.cu
+struct LzState {
+  double* alpha;   // [t][steps]
+  double* beta;    // [t][steps]
+  double* a_cur;   // [t]
+  double* h;       // [steps][t]
+  double* nrm;     // [t]
+  int* active;     // [t]
+  int* count;      // [t]
+  int* done;       // [1]
+};
+void lz_init(Context* c, const double* z, double* q0, int64_t n, int t, const double* zz_final,
+             LzState s);
+void lz_fin_alpha(Context* c, const double* part, int nblk, int t, int j, int steps, LzState s);
+void lz_update1(Context* c, double* w, const double* q, const double* qprev, int64_t n, int t,
+                int j, int steps, LzState s);
+void lz_multidot(Context* c, const double* basis, int64_t stride, int nb, const double* w,
+                 int64_t n, int t, double* part, const int* done);
+void lz_fin_h(Context* c, const double* part, int nblk, int nb, int t, LzState s);
+void lz_update2(Context* c, double* w, const double* basis, int64_t stride, int nb, int64_t n,
+                int t, LzState s, double* part);
+void lz_fin_beta(Context* c, const double* part, int nblk, int t, int j, int steps, LzState s);
+void lz_normalize(Context* c, const double* w, double* qnext, int64_t n, int t, LzState s);
+void quad_dot(Context* c, const double* a, const double* b, int64_t n, int t, double* part,
+              double* out);
+}  // namespace vec
+
+}  // namespace lgp

@@ -1,0 +1,509 @@
+// AOT (nvcc, sm_100a) FP64 vector kernels of the device-resident solver loops.
+//
+// All vectors are n x t row-major (the t right-hand sides / probes of one
+// point contiguous). Column reductions are deterministic: a fixed
+// (n, t) -> block partition, a fixed per-thread stride order, an in-order
+// shared-memory combine, and a single-block in-order final sum. Scalar state
+// (step sizes, residuals, activity masks) is written only by single-block
+// "fin" kernels and read by the following launches, so no kernel races with
+// itself. Every kernel returns immediately once the device `done` flag is
+// set, which lets the host enqueue iterations ahead without syncing.
+//
+// Update formulas use explicit _rn intrinsics to keep the reference's
+// rounding sequence (no FMA contraction): x += step*p, r -= step*ap,
+// p = p*beta + r (solvers.py:115-121); w = w - a*q, w -= b*q_prev,
+// w -= B^T (B w) (solvers.py:143-147).
+#include <cuda_runtime.h>
+
+#include "lgp_internal.h"
+
+namespace lgp {
+namespace vec {
+namespace {
+
+constexpr int kMaxBlocks = 512;
+constexpr int kRowsPerBlock = 2048;
+
+inline int reduce_bd(int t) { return t * (256 / t); }
+
+__device__ __forceinline__ bool is_done(const int* done) { return done != nullptr && *done; }
+
+// block partial of sum_i a[i][c]*b[i][c] over this block's row range -> part[blk][c]
+__device__ __forceinline__ void block_colsum(double v, int t, double* part_row, double* sm) {
+  const int tid = threadIdx.x;
+  const int bd = blockDim.x;
+  sm[tid] = v;
+  __syncthreads();
+  if (tid < t) {
+    double s = 0.0;
+    for (int k = tid; k < bd; k += t) s += sm[k];
+    part_row[tid] = s;
+  }
+  __syncthreads();
+}
+
+__global__ void k_dot_partial(const double* __restrict__ a, const double* __restrict__ b,
+                              long long n, int t, long long chunk, double* part, const int* done) {
+  __shared__ double sm[256];
+  if (is_done(done)) return;
+  const int tid = threadIdx.x;
+  const int c = tid % t;
+  const int stride = blockDim.x / t;
+  const long long r0 = (long long)blockIdx.x * chunk;
+  long long r1 = r0 + chunk;
+  if (r1 > n) r1 = n;
+  double s = 0.0;
+  if (tid < stride * t)
+    for (long long i = r0 + tid / t; i < r1; i += stride) s = fma(a[i * t + c], b[i * t + c], s);
+  block_colsum(s, t, part + (size_t)blockIdx.x * t, sm);
+}
+
+__global__ void k_dot_final(const double* part, int nblk, int t, double* out, const int* done) {
+  if (is_done(done)) return;
+  for (int c = threadIdx.x; c < t; c += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[(size_t)b * t + c];
+    out[c] = s;
+  }
+}
+
+__global__ void k_pack(const double* __restrict__ V, long long n, int t, long long n_pad, int tb,
+                       int n_pass, double* __restrict__ out, const int* done) {
+  if (is_done(done)) return;
+  const long long total = (long long)n_pass * n_pad * tb;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int cc = (int)(e % tb);
+    const long long j = (e / tb) % n_pad;
+    const int p = (int)(e / ((long long)tb * n_pad));
+    const int c = p * tb + cc;
+    out[e] = (j < n && c < t) ? V[j * t + c] : 0.0;
+  }
+}
+
+__global__ void k_epilogue(const double* __restrict__ partial, int n_seg, int n_pass,
+                           long long rows_pad, int tb, long long n_rows, int t, double scale,
+                           double noise, const double* __restrict__ noise_v,
+                           double* __restrict__ out, const int* done) {
+  if (is_done(done)) return;
+  const long long total = n_rows * t;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / t;
+    const int c = (int)(e % t);
+    const int p = c / tb, cc = c % tb;
+    double s = 0.0;
+    for (int g = 0; g < n_seg; ++g) s += partial[(((long long)g * n_pass + p) * rows_pad + i) * tb + cc];
+    double o = __dmul_rn(scale, s);
+    if (noise_v != nullptr && noise != 0.0) o = __dadd_rn(o, __dmul_rn(noise, noise_v[e]));
+    out[e] = o;
+  }
+}
+
+__global__ void k_fill(double* p, long long n, double v) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    p[e] = v;
+}
+
+// ------------------------------------------------------------------ CG
+__global__ void k_cg_init_vecs(const double* __restrict__ b, double* x, double* r, double* p,
+                               long long total) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double v = b[e];
+    x[e] = 0.0;
+    r[e] = v;
+    p[e] = v;
+  }
+}
+
+__global__ void k_cg_init_scalars(const double* bb, int t, double rel_tol, CgState s) {
+  if (threadIdx.x == 0) {
+    *s.status = 0;
+    *s.bad_col = -1;
+  }
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < t; c += blockDim.x) {
+    const double bn = sqrt(bb[c]);
+    s.tol[c] = rel_tol * bn;
+    s.rs[c] = bb[c];
+    s.step[c] = 0.0;
+    s.beta[c] = 0.0;
+    s.iters[c] = 0;
+    s.res[c] = 0.0;
+    const int act = bn != 0.0;  // zero column: 0 iterations, residual 0 (solvers.py:100-101)
+    s.active[c] = act;
+    if (act) atomicOr(&any, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *s.done = any ? 0 : 1;
+}
+
+__global__ void k_cg_fin_pap(const double* part, int nblk, int t, CgState s) {
+  if (*s.done) return;
+  for (int c = threadIdx.x; c < t; c += blockDim.x) {
+    double pap = 0.0;
+    for (int b = 0; b < nblk; ++b) pap += part[(size_t)b * t + c];
+    if (s.active[c]) {
+      if (pap <= 0.0) {  // breakdown: operator not SPD (solvers.py:110-113)
+        *s.status = 1;
+        *s.bad_col = c;
+        *s.done = 1;
+      }
+      s.step[c] = s.rs[c] / pap;
+    }
+  }
+}
+
+__global__ void k_cg_update_xr(double* __restrict__ x, double* __restrict__ r,
+                               const double* __restrict__ p, const double* __restrict__ ap,
+                               long long n, int t, long long chunk, CgState s, double* part) {
+  __shared__ double sm[256];
+  if (*s.done) return;
+  const int tid = threadIdx.x;
+  const int c = tid % t;
+  const int stride = blockDim.x / t;
+  const long long r0 = (long long)blockIdx.x * chunk;
+  long long r1 = r0 + chunk;
+  if (r1 > n) r1 = n;
+  double acc = 0.0;
+  if (tid < stride * t) {
+    const bool act = s.active[c] != 0;
+    const double st = s.step[c];
+    for (long long i = r0 + tid / t; i < r1; i += stride) {
+      const long long e = i * t + c;
+      double rv = r[e];
+      if (act) {
+        x[e] = __dadd_rn(x[e], __dmul_rn(st, p[e]));
+        rv = __dsub_rn(rv, __dmul_rn(st, ap[e]));
+        r[e] = rv;
+      }
+      acc = fma(rv, rv, acc);
+    }
+  }
+  block_colsum(acc, t, part + (size_t)blockIdx.x * t, sm);
+}
+
+__global__ void k_cg_fin_rs(const double* part, int nblk, int t, int it, int max_iter,
+                            CgState s) {
+  if (*s.done) return;
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < t; c += blockDim.x) {
+    double rs_new = 0.0;
+    for (int b = 0; b < nblk; ++b) rs_new += part[(size_t)b * t + c];
+    if (!s.active[c]) continue;
+    const double nrm = sqrt(rs_new);
+    if (nrm <= s.tol[c] || it >= max_iter) {  // converged, or budget spent (reported)
+      s.iters[c] = it;
+      s.res[c] = nrm;
+      s.active[c] = 0;
+    } else {
+      s.beta[c] = rs_new / s.rs[c];
+      s.rs[c] = rs_new;
+      atomicOr(&any, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && !any) *s.done = 1;
+}
+
+__global__ void k_cg_update_p(double* __restrict__ p, const double* __restrict__ r, long long total,
+                              int t, CgState s) {
+  if (*s.done) return;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % t);
+    if (s.active[c]) p[e] = __dadd_rn(__dmul_rn(p[e], s.beta[c]), r[e]);
+  }
+}
+
+// ------------------------------------------------------------- Lanczos
+__global__ void k_lz_init(const double* __restrict__ z, double* __restrict__ q, long long total,
+                          int t, const double* zz) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % t);
+    q[e] = z[e] / sqrt(zz[c]);
+  }
+}
+
+__global__ void k_lz_init_scalars(const double* zz, int t, LzState s) {
+  for (int c = threadIdx.x; c < t; c += blockDim.x) {
+    s.active[c] = zz[c] > 0.0;
+    s.count[c] = 0;
+  }
+  if (threadIdx.x == 0) *s.done = 0;
+}
+
+__global__ void k_lz_fin_alpha(const double* part, int nblk, int t, int j, int steps, LzState s) {
+  if (*s.done) return;
+  for (int c = threadIdx.x; c < t; c += blockDim.x) {
+    double a = 0.0;
+    for (int b = 0; b < nblk; ++b) a += part[(size_t)b * t + c];
+    if (s.active[c]) {
+      s.alpha[(size_t)c * steps + j] = a;
+      s.a_cur[c] = a;
+      s.count[c] = j + 1;
+    }
+  }
+}
+
+__global__ void k_lz_update1(double* __restrict__ w, const double* __restrict__ q,
+                             const double* __restrict__ qprev, long long total, int t, int j,
+                             int steps, LzState s) {
+  if (*s.done) return;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % t);
+    if (!s.active[c]) {
+      w[e] = 0.0;
+      continue;
+    }
+    double v = __dsub_rn(w[e], __dmul_rn(s.a_cur[c], q[e]));
+    if (j > 0) v = __dsub_rn(v, __dmul_rn(s.beta[(size_t)c * steps + j - 1], qprev[e]));
+    w[e] = v;
+  }
+}
+
+// part[blk][k][c] = sum over this block's rows of basis[k][i][c] * w[i][c], k < nb
+__global__ void k_lz_multidot(const double* __restrict__ basis, long long stride_k, int nb,
+                              const double* __restrict__ w, long long n, int t, long long chunk,
+                              double* part, const int* done) {
+  __shared__ double sm[256];
+  if (is_done(done)) return;
+  const int tid = threadIdx.x;
+  const int c = tid % t;
+  const int stride = blockDim.x / t;
+  const long long r0 = (long long)blockIdx.x * chunk;
+  long long r1 = r0 + chunk;
+  if (r1 > n) r1 = n;
+  for (int k = 0; k < nb; ++k) {
+    const double* bk = basis + (size_t)k * stride_k;
+    double s = 0.0;
+    if (tid < stride * t)
+      for (long long i = r0 + tid / t; i < r1; i += stride) s = fma(bk[i * t + c], w[i * t + c], s);
+    block_colsum(s, t, part + ((size_t)blockIdx.x * nb + k) * t, sm);
+  }
+}
+
+__global__ void k_lz_fin_h(const double* part, int nblk, int nb, int t, LzState s) {
+  if (*s.done) return;
+  for (int e = threadIdx.x; e < nb * t; e += blockDim.x) {
+    double h = 0.0;
+    for (int b = 0; b < nblk; ++b) h += part[(size_t)b * nb * t + e];
+    s.h[e] = h;
+  }
+}
+
+__global__ void k_lz_update2(double* __restrict__ w, const double* __restrict__ basis,
+                             long long stride_k, int nb, long long n, int t, long long chunk,
+                             LzState s, double* part) {
+  __shared__ double sm[256];
+  if (*s.done) return;
+  const int tid = threadIdx.x;
+  const int c = tid % t;
+  const int stride = blockDim.x / t;
+  const long long r0 = (long long)blockIdx.x * chunk;
+  long long r1 = r0 + chunk;
+  if (r1 > n) r1 = n;
+  double acc = 0.0;
+  if (tid < stride * t) {
+    const bool act = s.active[c] != 0;
+    for (long long i = r0 + tid / t; i < r1; i += stride) {
+      const long long e = i * t + c;
+      double v = w[e];
+      if (act) {
+        double u = 0.0;
+        for (int k = 0; k < nb; ++k) u = fma(basis[(size_t)k * stride_k + e], s.h[k * t + c], u);
+        v = __dsub_rn(v, u);
+        w[e] = v;
+      }
+      acc = fma(v, v, acc);
+    }
+  }
+  block_colsum(acc, t, part + (size_t)blockIdx.x * t, sm);
+}
+
+__global__ void k_lz_fin_beta(const double* part, int nblk, int t, int j, int steps, LzState s) {
+  if (*s.done) return;
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < t; c += blockDim.x) {
+    double ss = 0.0;
+    for (int b = 0; b < nblk; ++b) ss += part[(size_t)b * t + c];
+    if (!s.active[c]) continue;
+    const double nb = sqrt(ss);
+    const double a = fabs(s.a_cur[c]);
+    if (nb <= 1e-12 * (a > 1.0 ? a : 1.0)) {  // invariant subspace (solvers.py:151-152)
+      s.active[c] = 0;
+    } else {
+      s.beta[(size_t)c * steps + j] = nb;
+      s.nrm[c] = nb;
+      atomicOr(&any, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && !any) *s.done = 1;
+}
+
+__global__ void k_lz_normalize(const double* __restrict__ w, double* __restrict__ q,
+                               long long total, int t, LzState s) {
+  if (*s.done) return;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % t);
+    q[e] = s.active[c] ? w[e] / s.nrm[c] : 0.0;
+  }
+}
+
+inline int grid_for(long long total, int bd = 256) {
+  long long g = (total + bd - 1) / bd;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+inline long long chunk_rows(long long n, int nblk) { return (n + nblk - 1) / nblk; }
+
+#define LGP_LAUNCH_CHECK(ctx)                 \
+  do {                                        \
+    ++(ctx)->launches;                        \
+    LGP_CUDA_CHECK(cudaGetLastError());       \
+  } while (0)
+
+}  // namespace
+
+int reduce_blocks(int64_t n, int t) {
+  (void)t;
+  long long b = (n + kRowsPerBlock - 1) / kRowsPerBlock;
+  if (b > kMaxBlocks) b = kMaxBlocks;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int tb, int n_pass,
+              double* out, const int* done) {
+  k_pack<<<grid_for((long long)n_pass * n_pad * tb), 256, 0, c->stream>>>(V, n, t, n_pad, tb,
+                                                                         n_pass, out, done);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void epilogue(Context* c, const double* partial, int n_seg, int n_pass, int64_t rows_pad, int tb,
+              int64_t n_rows, int t, double scale, double noise, const double* noise_v,
+              double* out, const int* done) {
+  k_epilogue<<<grid_for(n_rows * t), 256, 0, c->stream>>>(
+      partial, n_seg, n_pass, rows_pad, tb, n_rows, t, scale, noise, noise_v, out, done);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void dot_partial(Context* c, const double* a, const double* b, int64_t n, int t, double* part,
+                 const int* done) {
+  const int nb = reduce_blocks(n, t);
+  k_dot_partial<<<nb, reduce_bd(t), 0, c->stream>>>(a, b, n, t, chunk_rows(n, nb), part, done);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void dot_final(Context* c, const double* part, int nblk, int t, double* out, const int* done) {
+  k_dot_final<<<1, 256, 0, c->stream>>>(part, nblk, t, out, done);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void fill(Context* c, double* p, int64_t n, double v) {
+  k_fill<<<grid_for(n), 256, 0, c->stream>>>(p, n, v);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void cg_init(Context* c, const double* b, double* x, double* r, double* p, int64_t n, int t,
+             double rel_tol, const double* bb_final, CgState s) {
+  k_cg_init_vecs<<<grid_for(n * t), 256, 0, c->stream>>>(b, x, r, p, n * t);
+  LGP_LAUNCH_CHECK(c);
+  k_cg_init_scalars<<<1, 256, 0, c->stream>>>(bb_final, t, rel_tol, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void cg_fin_pap(Context* c, const double* part, int nblk, int t, CgState s) {
+  k_cg_fin_pap<<<1, 256, 0, c->stream>>>(part, nblk, t, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void cg_update_xr(Context* c, double* x, double* r, const double* p, const double* ap, int64_t n,
+                  int t, CgState s, double* part) {
+  const int nb = reduce_blocks(n, t);
+  k_cg_update_xr<<<nb, reduce_bd(t), 0, c->stream>>>(x, r, p, ap, n, t, chunk_rows(n, nb), s, part);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void cg_fin_rs(Context* c, const double* part, int nblk, int t, int it, int max_iter, CgState s) {
+  k_cg_fin_rs<<<1, 256, 0, c->stream>>>(part, nblk, t, it, max_iter, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void cg_update_p(Context* c, double* p, const double* r, int64_t n, int t, CgState s) {
+  k_cg_update_p<<<grid_for(n * t), 256, 0, c->stream>>>(p, r, n * t, t, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void lz_init(Context* c, const double* z, double* q0, int64_t n, int t, const double* zz_final,
+             LzState s) {
+  k_lz_init<<<grid_for(n * t), 256, 0, c->stream>>>(z, q0, n * t, t, zz_final);
+  LGP_LAUNCH_CHECK(c);
+  k_lz_init_scalars<<<1, 256, 0, c->stream>>>(zz_final, t, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void lz_fin_alpha(Context* c, const double* part, int nblk, int t, int j, int steps, LzState s) {
+  k_lz_fin_alpha<<<1, 256, 0, c->stream>>>(part, nblk, t, j, steps, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void lz_update1(Context* c, double* w, const double* q, const double* qprev, int64_t n, int t,
+                int j, int steps, LzState s) {
+  k_lz_update1<<<grid_for(n * t), 256, 0, c->stream>>>(w, q, qprev, n * t, t, j, steps, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void lz_multidot(Context* c, const double* basis, int64_t stride, int nb, const double* w,
+                 int64_t n, int t, double* part, const int* done) {
+  const int nblk = reduce_blocks(n, t);
+  k_lz_multidot<<<nblk, reduce_bd(t), 0, c->stream>>>(basis, stride, nb, w, n, t,
+                                                      chunk_rows(n, nblk), part, done);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void lz_fin_h(Context* c, const double* part, int nblk, int nb, int t, LzState s) {
+  k_lz_fin_h<<<1, 256, 0, c->stream>>>(part, nblk, nb, t, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void lz_update2(Context* c, double* w, const double* basis, int64_t stride, int nb, int64_t n,
+                int t, LzState s, double* part) {
+  const int nblk = reduce_blocks(n, t);
+  k_lz_update2<<<nblk, reduce_bd(t), 0, c->stream>>>(w, basis, stride, nb, n, t,
+                                                     chunk_rows(n, nblk), s, part);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void lz_fin_beta(Context* c, const double* part, int nblk, int t, int j, int steps, LzState s) {
+  k_lz_fin_beta<<<1, 256, 0, c->stream>>>(part, nblk, t, j, steps, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void lz_normalize(Context* c, const double* w, double* qnext, int64_t n, int t, LzState s) {
+  k_lz_normalize<<<grid_for(n * t), 256, 0, c->stream>>>(w, qnext, n * t, t, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void quad_dot(Context* c, const double* a, const double* b, int64_t n, int t, double* part,
+              double* out) {
+  dot_partial(c, a, b, n, t, part, nullptr);
+  dot_final(c, part, reduce_blocks(n, t), t, out, nullptr);
+}
+
+}  // namespace vec
+}  // namespace lgp

@@ -1,0 +1,149 @@
+"""Exact GP regression through the matrix-free CG path (minigp/models.py, CG branch).
+
+``gp_fit(..., strategy="cg")``, ``gp_predict`` and ``log_marginal_likelihood``
+keep the reference's signatures, validation and fitted-state fields
+(models.py:52-72, 143-266). The operator is always the GPU-resident
+:class:`KernelOperator` (the reference switches to a dense Gram below
+N = 2048, models.py:174-182; the two operators are the same matrix, only
+rounding differs), so:
+
+* fit        -> one device CG solve (lgp_cg)
+* predict    -> mean from the fused cross matvec K(X*, X) alpha; variance from
+                k* formed on the device and ONE multi-RHS device CG with one
+                column per test point (the reference runs T separate solves,
+                models.py:239-246)
+* evidence   -> y.alpha + SLQ log-det with all probes in lockstep (lgp_lanczos)
+
+The Cholesky, SKI and sparse-variational strategies are outside this
+drop-in's scope and raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import DimensionMismatchError
+from .kernels import is_stationary
+from .linalg import as_matrix, as_vector, tracked
+from .solvers import CgConfig, KernelOperator, cg_solve
+
+AUTO_CHOLESKY_MAX = 4000  # models.py:43
+DENSE_OPERATOR_MAX = 2048  # models.py:44 (kept for reference; the device never densifies)
+CG_FIT_BLOCK = 32  # models.py:45
+FIT_CG_TOLERANCE = 1e-8  # models.py:46
+LOG_2PI = math.log(2.0 * math.pi)
+
+
+@dataclass(frozen=True)
+class ExactState:
+    """Fitted exact GP (models.py:52-72); ``operator`` holds the device operator."""
+
+    x_train: np.ndarray
+    y_train: np.ndarray
+    kernel: object
+    noise: float
+    strategy: str
+    alpha: np.ndarray
+    factor: object = None
+    gram_y: np.ndarray | None = None
+    ski: object = None
+    cg_iterations: int | None = None
+    cg_final_residual: float | None = None
+    cg_config: CgConfig | None = None
+    operator: KernelOperator | None = field(default=None, repr=False, compare=False)
+
+
+def _check_noise(noise):
+    noise = float(noise)
+    if not math.isfinite(noise) or noise <= 0:
+        raise ValueError("noise variance must be positive and finite")
+    return noise
+
+
+def _resolve_strategy(strategy, n, d, kernel):
+    s = str(strategy).lower()
+    if s == "auto":  # models.py:130-140
+        if n <= AUTO_CHOLESKY_MAX:
+            s = "cholesky"
+        elif d == 1 and is_stationary(kernel):
+            s = "ski"
+        else:
+            s = "cg"
+    if s not in ("cholesky", "cg", "ski"):
+        raise ValueError(f"unknown strategy {strategy!r}")
+    if s != "cg":
+        raise NotImplementedError(
+            f"strategy {s!r} is outside this drop-in's scope: only the matrix-free CG path "
+            "is provided (pass strategy='cg')")
+    return s
+
+
+def gp_fit(x, y, kernel, noise, strategy="auto", *, cg_config=None, grid_size=None):
+    """Fit an exact GP with the device CG solver (models.py:143-200)."""
+    x = as_matrix(x, "X")
+    y = as_vector(y, "y")
+    n, d = x.shape
+    if y.shape[0] != n:
+        raise DimensionMismatchError(f"y has length {y.shape[0]}, X has {n} rows")
+    if n < 1:
+        raise DimensionMismatchError("need at least one training point")
+    noise = _check_noise(noise)
+    resolved = _resolve_strategy(strategy, n, d, kernel)
+    cfg = cg_config if cg_config is not None else CgConfig(rel_tolerance=FIT_CG_TOLERANCE)
+    op = KernelOperator(kernel, x, noise)
+    res = cg_solve(op, y, cfg)
+    return ExactState(x, y, kernel, noise, resolved, res.x, cg_iterations=res.iterations,
+                      cg_final_residual=res.final_residual, cg_config=cfg, operator=op)
+
+
+def _operator(state):
+    """The fitted K_y operator (models.py:203-213)."""
+    if state.operator is not None:
+        return state.operator
+    return KernelOperator(state.kernel, state.x_train, state.noise)
+
+
+def gp_predict(state, x_star):
+    """Posterior mean and latent variance (models.py:216-250)."""
+    x_star = as_matrix(x_star, "X*")
+    if x_star.shape[1] != state.x_train.shape[1]:
+        raise DimensionMismatchError(
+            f"test inputs have {x_star.shape[1]} columns, training had {state.x_train.shape[1]}")
+    t = x_star.shape[0]
+    if t == 0:
+        return tracked(np.zeros(0)), tracked(np.zeros(0))
+    op = _operator(state)
+    lib, ctx = _lib.lib(), op.ctx
+    test = _lib.DevicePoints(ctx, x_star)
+    alpha = np.ascontiguousarray(state.alpha)
+    mean = np.empty(t)
+    _lib.check(lib.lgp_matvec(ctx.handle, op.prog.handle, test.handle, op.points.handle, 0.0,
+                              _lib.vptr(alpha), 1, _lib.vptr(mean), 0))
+    prior = np.empty(t)
+    _lib.check(lib.lgp_diag(ctx.handle, op.prog.handle, test.handle, _lib.vptr(prior), 0))
+    cfg = state.cg_config if state.cg_config is not None else CgConfig()
+    quad = np.empty(t)
+    iters = np.zeros(t, dtype=np.int32)
+    res = np.zeros(t)
+    mi = 0 if cfg.max_iterations is None else int(cfg.max_iterations)
+    _lib.check(lib.lgp_predict_quad(ctx.handle, op.prog.handle, op.points.handle, test.handle,
+                                    state.noise, cfg.rel_tolerance, mi, _lib.dptr(quad),
+                                    _lib.iptr(iters), _lib.dptr(res)))
+    var = prior - quad
+    np.maximum(var, 0.0, out=var)
+    return tracked(mean), tracked(var)
+
+
+def log_marginal_likelihood(state, seed=0):
+    """-1/2 (y.alpha + log det K_y + N log 2 pi), log-det by device SLQ (models.py:253-266)."""
+    from .solvers import slq_logdet
+
+    n = state.y_train.shape[0]
+    quad = float(state.y_train @ state.alpha)
+    cfg = state.cg_config if state.cg_config is not None else CgConfig()
+    ld = slq_logdet(_operator(state), n, cfg, seed=seed)
+    return -0.5 * (quad + ld + n * LOG_2PI)
