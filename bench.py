@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the matrix-free K_y.V hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg4]
+
+One *step* = one (K + noise I) V product over the whole synthetic workload of
+the config (default cfg4: RBF(0.5), N=100,000, D=8, V = the t=16 SLQ probe
+vectors), with X and V resident in HBM. Under torchrun (N>1) the rows of K are
+sharded over the ranks and each step ends with the library's NCCL all-gather
+of the product slices, so every rank holds the full product (strong scaling:
+total work fixed). Device time per step from CUDA events on the library's
+stream, L2 flushed (256 MiB memset) before every timed step, summed over the
+K steps, max over ranks.
+
+Also reported: `e2e` (the same metric through the public Python API with
+pinned host buffers, H2D of X and V and D2H of the product inside the timed
+region), the CG solve time (t=1 alpha solve, tol 1e-8, max_iter min(N,1000))
+and the SLQ log-det time (16 probes x 50 Lanczos steps), the roofline of the
+fused K1 kernel (per-launch CUDA events) and the CPU baseline (the pinned
+oracle port of the reference, rank 0 only).
+
+`--impl reference` times the reference's own CPU algorithm (oracle port of
+minigp's matrix_free_matvec; the reference is pure Python) on a bounded row
+sample of the same workload per step, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "kernel-matvec Gentries/s and CG solve time at N=100k, D=8, 1/2/4/8 B200"
+UNIT = "Gentries/s"
+SM_COUNT = 148
+FP32_LANES = 128
+SFU_PER_SM = 16
+
+
+def flops_per_entry(kernel_expr, d, t):
+    """Algorithmic work per kernel entry: distance 3D, leaf
+    transform, +2t for the contraction. Transcendentals are SFU ops, not flops."""
+    if kernel_expr.startswith("(rbf"):
+        return 3 * d + 1 + 2 * t, 1
+    if kernel_expr.startswith("(matern52"):
+        return 3 * d + 5 + 2 * t, 2
+    if kernel_expr.startswith("(matern32"):
+        return 3 * d + 3 + 2 * t, 2
+    if kernel_expr.startswith("(+ (scale 1.0 (rbf"):  # cfg3 composite
+        return 3 * d + 1 + 4 * d + 1 + 3 + 2 * t, 2 + d
+    return 3 * d + 2 * t, 1
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def dist_setup(world):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo")
+    return dist
+
+
+def max_over_ranks(dist, value):
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([float(value)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(cfg, x, seconds=12.0):
+    """Oracle port of the reference matvec (block=32 fit path, one RHS column)
+    on a row subset of the same workload; extrapolated as entries/s."""
+    from oracle import gp_oracle as O
+
+    nodes = O.parse_tree(cfg["kernel"])
+    v = np.random.default_rng(1).standard_normal(cfg["n"])
+    rows = 1024 if cfg["n"] >= 50_000 else min(cfg["n"], 4096)
+    done, elapsed, reps = 0, 0.0, 0
+    while elapsed < seconds or reps < 2:
+        r0 = (reps * rows) % max(cfg["n"] - rows, 1)
+        t0 = time.perf_counter()
+        O.matvec(nodes, x, cfg["noise"], v, block=32, row_range=(r0, r0 + rows))
+        elapsed += time.perf_counter() - t0
+        done += rows * cfg["n"]
+        reps += 1
+    try:
+        import threadpoolctl
+
+        threads = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    return {"value": done / elapsed / 1e9, "unit": UNIT, "cores": int(threads),
+            "kind": "port",
+            "sample": f"{reps} x {rows}-row slabs x all {cfg['n']} columns, t=1 (reference has no "
+                      f"multi-RHS path: t columns cost t x), block=32, FP64 NumPy/OpenBLAS "
+                      f"({threads} BLAS threads, ufuncs single-threaded), {elapsed:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU algorithm (oracle port), rank 0 only."""
+    if rank != 0:
+        return 0
+    from oracle import gp_oracle as O
+
+    cfg = dict(O.CONFIGS[args.config])
+    x, _ = O.synthetic(cfg["n"], cfg["d"])
+    t = cfg["t"]
+    z = O.probes(cfg["n"], t)
+    nodes = O.parse_tree(cfg["kernel"])
+    rows = 64 if cfg["n"] >= 50_000 else min(cfg["n"], 512)
+    times = []
+    for s in range(args.warmup + args.steps):
+        r0 = (s * 997 * rows) % max(cfg["n"] - rows, 1)
+        t0 = time.perf_counter()
+        O.matvec(nodes, x, cfg["noise"], z, block=32, row_range=(r0, r0 + rows))
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = args.steps * rows * cfg["n"] * t / total / 1e9
+    try:
+        import threadpoolctl
+
+        threads = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    sample = (f"per step: {rows}-row slab of the {cfg['n']}x{cfg['n']} operator x {t} RHS columns "
+              f"(each column a separate reference matvec, block=32)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args.config, cfg),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(threads), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(name, cfg):
+    return {"workload": f"{name}: (K+{cfg['noise']}I)V, kernel {cfg['kernel']}, N={cfg['n']}, "
+                        f"D={cfg['d']}, t={cfg['t']} SLQ probe vectors",
+            "n": cfg["n"], "d": cfg["d"], "t": cfg["t"], "kernel": cfg["kernel"],
+            "noise": cfg["noise"], "parallelism": "row-sharded K, NCCL all-gather",
+            "l2": "flushed (256 MiB memset) before every timed step"}
+
+
+def run_ours(args, rank, world):
+    import ctypes as C
+
+    import paper_2605_17898_b200 as G
+    from paper_2605_17898_b200 import _lib, distributed
+    from oracle import gp_oracle as O  # input recipe + CPU baseline only
+
+    dist = dist_setup(world)
+    ctx = distributed.init() if world > 1 else _lib.default_context()
+    lib = _lib.lib()
+    cfg = dict(O.CONFIGS[args.config])
+    n, d, t = cfg["n"], cfg["d"], cfg["t"]
+    x, y = O.synthetic(n, d)
+    z = np.ascontiguousarray(O.probes(n, t))
+    kernel = G.parse_kernel(cfg["kernel"])
+    prog = G.kernels.program(kernel)
+    pts = _lib.DevicePoints(ctx, x)
+    dv, do = C.c_void_p(), C.c_void_p()
+    _lib.check(lib.lgp_device_alloc(ctx.handle, z.nbytes, C.byref(dv)))
+    _lib.check(lib.lgp_device_alloc(ctx.handle, z.nbytes, C.byref(do)))
+    _lib.check(lib.lgp_memcpy_h2d(ctx.handle, dv, _lib.vptr(z), z.nbytes))
+
+    def step():
+        _lib.check(lib.lgp_matvec(ctx.handle, prog.handle, pts.handle, pts.handle, cfg["noise"],
+                                  dv, t, do, _lib.DEVICE_PTRS))
+
+    ctx.set_profile(True)
+    for _ in range(args.warmup):
+        ctx.flush_l2()
+        step()
+    ctx.k1_profile(reset=True)
+    if dist:
+        dist.barrier()
+    ctx.sync()
+    clocks = ClockSampler(ctx.device)
+    clocks.start()
+    launches0 = ctx.launches()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        ctx.flush_l2()
+        ctx.timer_start()
+        step()
+        total_ms += ctx.timer_stop()
+    launches = ctx.launches() - launches0
+    ctx.sync()
+    if dist:
+        dist.barrier()
+    k1_ms, k1_n = ctx.k1_profile(reset=True)
+    total_ms = max_over_ranks(dist, total_ms)
+    value = n * n * t * args.steps / (total_ms * 1e-3) / 1e9
+
+    # parity spot check of the timed product (rows owned by rank 0), vs the oracle
+    out = np.empty_like(z)
+    _lib.check(lib.lgp_memcpy_d2h(ctx.handle, _lib.vptr(out), do, z.nbytes))
+    r0 = n // 2
+    want = O.matvec(O.parse_tree(cfg["kernel"]), x, cfg["noise"], z[:, :2], block=32,
+                    row_range=(r0, r0 + 64))
+    parity = float(np.linalg.norm(out[r0:r0 + 64, :2] - want) / np.linalg.norm(want))
+
+    # e2e: public API call with pinned host buffers (H2D of X, V; D2H of the product)
+    hx, hv = C.c_void_p(), C.c_void_p()
+    _lib.check(lib.lgp_host_alloc(x.nbytes, C.byref(hx)))
+    _lib.check(lib.lgp_host_alloc(z.nbytes, C.byref(hv)))
+    px = np.ctypeslib.as_array(C.cast(hx, C.POINTER(C.c_double)), shape=x.shape)
+    pv = np.ctypeslib.as_array(C.cast(hv, C.POINTER(C.c_double)), shape=z.shape)
+    px[...] = x
+    pv[...] = z
+    for _ in range(2):
+        G.matrix_free_matvec(kernel, px, cfg["noise"], pv)
+    if dist:
+        dist.barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        res = G.matrix_free_matvec(kernel, px, cfg["noise"], pv)
+    e2e_s = max_over_ranks(dist, time.perf_counter() - t0)
+    del res
+    e2e = {"value": n * n * t * e2e_steps / e2e_s / 1e9, "unit": UNIT,
+           "h2d_bytes_per_step": int(x.nbytes + z.nbytes), "d2h_bytes_per_step": int(z.nbytes),
+           "ms_per_step": e2e_s / e2e_steps * 1e3,
+           "path": "paper_2605_17898_b200.matrix_free_matvec(kernel, X, noise, V) -> lgp_matvec"}
+
+    # CG solve (alpha) and SLQ log-det through the device solver loops
+    solve = {}
+    if not args.no_solve:
+        op = G.KernelOperator(kernel, x, cfg["noise"], ctx=ctx)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        xs, iters, resid = op.cg(y, 1e-8, None)
+        cg_s = max_over_ranks(dist, time.perf_counter() - t0)
+        k1_cg_ms, k1_cg_n = ctx.k1_profile(reset=True)
+        t0 = time.perf_counter()
+        ld = G.slq_logdet(op, n, G.CgConfig(probes=t if t > 1 else 16, lanczos_steps=50), seed=0)
+        slq_s = max_over_ranks(dist, time.perf_counter() - t0)
+        k1_slq_ms, k1_slq_n = ctx.k1_profile(reset=True)
+        solve = {"cg_solve": {"ms": cg_s * 1e3, "iterations": int(iters[0]),
+                              "final_residual": float(resid[0]), "rel_tolerance": 1e-8,
+                              "k1_ms_per_matvec": k1_cg_ms / max(k1_cg_n, 1)},
+                 "slq_logdet": {"ms": slq_s * 1e3, "probes": t if t > 1 else 16,
+                                "lanczos_steps": 50, "logdet": ld,
+                                "k1_ms_per_step": k1_slq_ms / max(k1_slq_n, 1)}}
+    clk = clocks.stop()
+
+    if rank != 0:
+        return 0
+    pk = measured_peaks()
+    f_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    fp32_peak = 2 * FP32_LANES * SM_COUNT * f_mhz * 1e6 / 1e12  # TFLOP/s
+    flops, sfu = flops_per_entry(cfg["kernel"], d, t)
+    k1_avg_ms = k1_ms / max(k1_n, 1)
+    rows_local = -(-n // world)
+    achieved = rows_local * n * flops / (k1_avg_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(args.config)
+    except Exception:
+        pass
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": traffic,
+                "kernel": "lgp_matvec (fused K1)", "k1_ms_per_launch": k1_avg_ms,
+                "flops_per_entry": flops, "sfu_per_entry": sfu,
+                "peak_source": f"derived: 2 x {FP32_LANES} FP32 lanes x {SM_COUNT} SMs x "
+                               f"{f_mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)",
+                "sfu_frac": rows_local * n * sfu / (k1_avg_ms * 1e-3)
+                            / (SFU_PER_SM * SM_COUNT * f_mhz * 1e6)}
+    if clk.get("sm_mhz"):
+        roofline["frac_at_observed_clock"] = achieved / (fp32_peak * clk["sm_mhz"] / f_mhz)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 entries / f64 accumulate", "data": "synthetic",
+            "config": workload_config(args.config, cfg),
+            "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk, "parity_rel_l2": parity}
+    line.update(solve)
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, x)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -95,6 +95,10 @@ int lgp_ctx_destroy(lgp_ctx* ctx);
 int lgp_ctx_sync(lgp_ctx* ctx);
 /* number of kernels this library has launched on the context (for bench) */
 int lgp_ctx_launch_count(lgp_ctx* ctx, uint64_t* out);
+/* Per-launch CUDA-event timing of the fused K1 matvec kernel (on its own
+ * stream): total device ms and launch count since the last reset. */
+int lgp_ctx_set_profile(lgp_ctx* ctx, int on);
+int lgp_ctx_profile(lgp_ctx* ctx, double* k1_ms_total, uint64_t* k1_launches, int reset);
 /* CUDA-event timer on the context's stream */
 int lgp_timer_start(lgp_ctx* ctx);
 int lgp_timer_stop(lgp_ctx* ctx, float* ms);

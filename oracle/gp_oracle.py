@@ -361,7 +361,7 @@ def predict(nodes, x, noise, alpha, xs, rel_tol=FIT_CG_TOLERANCE, max_iter=None)
     app = operator(nodes, x, noise)
     quad = np.empty(xs.shape[0])
     for j in range(xs.shape[0]):
-        col = np.ascontiguousarray(kstar[:, j])
+        col = kstar[:, j]  # strided view, as models.py:243 (affects dot rounding)
         sol = cg(app, col, rel_tol, max_iter)[0]
         quad[j] = col @ sol
     var = prior - quad

@@ -50,6 +50,8 @@ _SIGS = {
     "lgp_ctx_destroy": ([_P], C.c_int),
     "lgp_ctx_sync": ([_P], C.c_int),
     "lgp_ctx_launch_count": ([_P, C.POINTER(C.c_uint64)], C.c_int),
+    "lgp_ctx_set_profile": ([_P, C.c_int], C.c_int),
+    "lgp_ctx_profile": ([_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int], C.c_int),
     "lgp_timer_start": ([_P], C.c_int),
     "lgp_timer_stop": ([_P, C.POINTER(C.c_float)], C.c_int),
     "lgp_device_alloc": ([_P, C.c_size_t, C.POINTER(_P)], C.c_int),
@@ -162,6 +164,15 @@ class Context:
         n = C.c_uint64()
         check(lib().lgp_ctx_launch_count(self.handle, C.byref(n)))
         return n.value
+
+    def set_profile(self, on=True):
+        check(lib().lgp_ctx_set_profile(self.handle, 1 if on else 0))
+
+    def k1_profile(self, reset=True):
+        """(total device ms, launches) of the fused K1 kernel since the last reset."""
+        ms, n = C.c_double(), C.c_uint64()
+        check(lib().lgp_ctx_profile(self.handle, C.byref(ms), C.byref(n), 1 if reset else 0))
+        return ms.value, n.value
 
     def timer_start(self):
         check(lib().lgp_timer_start(self.handle))

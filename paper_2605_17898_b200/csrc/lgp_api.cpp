@@ -149,6 +149,11 @@ int lgp_ctx_destroy(lgp_ctx* ctx) {
   for (auto& kv : ctx->modules)
     if (kv.second->mod) drv::ModuleUnload(kv.second->mod);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+  for (auto& ev : ctx->ev_pending) ctx->ev_pool.push_back(ev);
+  for (auto& ev : ctx->ev_pool) {
+    cudaEventDestroy(ev.first);
+    cudaEventDestroy(ev.second);
+  }
   comm_destroy(ctx->comm);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
@@ -168,6 +173,35 @@ int lgp_ctx_sync(lgp_ctx* ctx) {
 int lgp_ctx_launch_count(lgp_ctx* ctx, uint64_t* out) {
   API_BEGIN
   *out = ctx->launches;
+  API_END
+}
+
+int lgp_ctx_set_profile(lgp_ctx* ctx, int on) {
+  API_BEGIN
+  std::lock_guard<std::recursive_mutex> g(ctx->mu);
+  ctx->profile = on != 0;
+  API_END
+}
+
+int lgp_ctx_profile(lgp_ctx* ctx, double* k1_ms_total, uint64_t* k1_launches, int reset) {
+  API_BEGIN
+  std::lock_guard<std::recursive_mutex> g(ctx->mu);
+  ctx->activate();
+  LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  for (auto& ev : ctx->ev_pending) {
+    float ms = 0.f;
+    LGP_CUDA_CHECK(cudaEventElapsedTime(&ms, ev.first, ev.second));
+    ctx->prof_ms += ms;
+    ctx->prof_count += 1;
+    ctx->ev_pool.push_back(ev);
+  }
+  ctx->ev_pending.clear();
+  if (k1_ms_total) *k1_ms_total = ctx->prof_ms;
+  if (k1_launches) *k1_launches = ctx->prof_count;
+  if (reset) {
+    ctx->prof_ms = 0.0;
+    ctx->prof_count = 0;
+  }
   API_END
 }
 

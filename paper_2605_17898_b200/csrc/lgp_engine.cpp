@@ -129,7 +129,22 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
   a.n_tiles = n_tiles;
   const int64_t grid = (int64_t)n_rb * n_seg * n_pass;
   if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (ctx->profile) {
+    if (ctx->ev_pool.empty()) {
+      LGP_CUDA_CHECK(cudaEventCreate(&ev.first));
+      LGP_CUDA_CHECK(cudaEventCreate(&ev.second));
+    } else {
+      ev = ctx->ev_pool.back();
+      ctx->ev_pool.pop_back();
+    }
+    LGP_CUDA_CHECK(cudaEventRecord(ev.first, ctx->stream));
+  }
   launch(ctx, mod->matvec, (unsigned)grid, 1, plan.tune.threads, plan.smem_bytes, &a);
+  if (ctx->profile) {
+    LGP_CUDA_CHECK(cudaEventRecord(ev.second, ctx->stream));
+    ctx->ev_pending.push_back(ev);
+  }
   vec::epilogue(ctx, partial, n_seg, n_pass, n_rows_pad, tb, n_rows, t, plan.root_scale, noise,
                 noise_v, out_dev, done);
 }

@@ -133,6 +133,12 @@ struct Context {
   uint64_t launches = 0;
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
+  // K1 timing (lgp_ctx_set_profile): event pairs around every fused-matvec
+  // launch, on the launching stream
+  bool profile = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_pending;
+  double prof_ms = 0.0;
+  uint64_t prof_count = 0;
 
   void* scratch_get(const std::string& name, size_t bytes);  // grow-only
   void activate();  // cudaSetDevice for the calling thread

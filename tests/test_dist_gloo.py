@@ -1,0 +1,106 @@
+"""World-size-2 (gloo, CPU) coverage of the multi-GPU path's host logic:
+the library's row partition, the NCCL unique-id exchange used by
+distributed.init(), and the sharded-CG schedule (local rows of K.p ->
+all-gather -> redundant FP64 updates) reproducing the unsharded reference CG."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import ctypes as C
+
+        import torch
+        from oracle import gp_oracle as O
+        from paper_2605_17898_b200 import _lib, distributed
+
+        res = {}
+        # 1. partition from the C ABI
+        n = 1001
+        r0, r1 = distributed.partition(n, world, rank)
+        res["part"] = (r0, r1)
+        # 2. NCCL id exchange (what distributed.init does before lgp_ctx_create)
+        obj = [None]
+        if rank == 0:
+            buf = C.create_string_buffer(128)
+            try:
+                _lib.check(_lib.lib().lgp_comm_unique_id(buf))
+                obj[0] = buf.raw
+            except Exception as exc:  # NCCL not loadable here
+                obj[0] = f"ERR {exc}".encode()
+        dist.broadcast_object_list(obj, src=0)
+        res["id"] = obj[0]
+        # 3. sharded CG schedule on the oracle
+        rng = np.random.default_rng(3)
+        x = rng.random((n, 3))
+        b = rng.standard_normal(n)
+        nodes = O.parse_tree("(scale 1.2 (matern52 0.6))")
+        S = -(-n // world)
+
+        def sharded_apply(p):
+            local = O.matvec(nodes, x, 0.1, p, block=64, row_range=(r0, r1))
+            buf = torch.zeros(S, dtype=torch.float64)
+            buf[: r1 - r0] = torch.from_numpy(local)
+            parts = [torch.zeros(S, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(parts, buf)
+            full = torch.cat(parts).numpy()[:n]
+            return full
+
+        xs, it, rr = O.cg(sharded_apply, b, 1e-10)
+        res["cg"] = (xs, it, rr)
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_partition_id_and_sharded_cg():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # partition covers [0, n) without overlap
+    assert out[0]["part"] == (0, 501) and out[1]["part"] == (501, 1001)
+    # every rank received the same id bytes
+    assert out[0]["id"] == out[1]["id"]
+    if not out[0]["id"].startswith(b"ERR"):
+        assert len(out[0]["id"]) == 128
+    # both ranks hold identical CG state, equal to the unsharded reference CG
+    from oracle import gp_oracle as O
+
+    rng = np.random.default_rng(3)
+    x = rng.random((1001, 3))
+    b = rng.standard_normal(1001)
+    nodes = O.parse_tree("(scale 1.2 (matern52 0.6))")
+    ref = O.cg(lambda v: O.matvec(nodes, x, 0.1, v, block=64), b, 1e-10)
+    x0, it0, r0 = out[0]["cg"]
+    x1, it1, r1 = out[1]["cg"]
+    np.testing.assert_array_equal(x0, x1)
+    assert it0 == it1 == ref[1]
+    np.testing.assert_allclose(x0, ref[0], rtol=0, atol=1e-9 * np.abs(ref[0]).max())

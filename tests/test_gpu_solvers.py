@@ -1,0 +1,122 @@
+"""GPU parity of the device-resident CG / SLQ loops and of the model layer
+against the reference's golden outputs. Bars (north_star): predictive mean and
+log marginal likelihood within 1e-4 relative of the reference at its own
+tolerance / iteration budget; CG-path variance within the reference's own
+cross-path tolerance 3e-3 (test_models.py:186-192)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2605_17898_b200 as G
+from conftest import GOLDEN, golden, rel_l2
+from oracle import gp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def small_inputs(n, d, seed):
+    rng = np.random.default_rng(seed)
+    return rng.random((n, d)), rng.standard_normal(n)
+
+
+def test_cg_golden(gpu_ctx):
+    g = golden("cg_small.npz")
+    for ci in range(4):
+        n, d, seed = (int(a) for a in g[f"case_{ci}"])
+        x, b = small_inputs(n, d, seed)
+        k = G.parse_kernel(str(g[f"tree_{ci}"]))
+        tol = float(g[f"tol_{ci}"])
+        op = G.KernelOperator(k, x, 0.1)
+        res = G.cg_solve(op, b, G.CgConfig(rel_tolerance=tol))
+        it_ref = int(g[f"it_{ci}"])
+        assert abs(res.iterations - it_ref) <= max(2, 0.15 * it_ref), (res.iterations, it_ref)
+        assert res.final_residual <= tol * np.linalg.norm(b) or res.iterations == min(n, 1000)
+        # solution vs the reference's solution
+        assert rel_l2(res.x, g[f"x_{ci}"]) <= 1e-4
+        # residual against the exact FP64 operator (test_models.py:97-105 style)
+        gram = O.gram(O.parse_tree(G.format_kernel(k)), x, x, same=True)
+        gram.flat[:: n + 1] += 0.1
+        assert np.linalg.norm(gram @ res.x - b) <= max(20 * tol, 1e-5) * np.linalg.norm(b)
+
+
+def test_cg_same_iteration_budget(gpu_ctx):
+    # equal, pinned iteration budgets: device and oracle after exactly k steps
+    x, b = small_inputs(800, 4, 21)
+    k = G.Matern52(0.5)
+    nodes = O.parse_tree(G.format_kernel(k))
+    for it in (5, 25):
+        cfg = G.CgConfig(rel_tolerance=1e-30, max_iterations=it)
+        res = G.cg_solve(G.KernelOperator(k, x, 0.1), b, cfg)
+        ref = O.cg(lambda v: O.matvec(nodes, x, 0.1, v), b, 1e-30, it)
+        assert res.iterations == it == ref[1]
+        assert rel_l2(res.x, ref[0]) <= 1e-5
+
+
+def test_cg_multi_rhs_and_edge_columns(gpu_ctx):
+    x, _ = small_inputs(600, 3, 31)
+    rng = np.random.default_rng(32)
+    B = rng.standard_normal((600, 5))
+    B[:, 2] = 0.0  # zero column: 0 iterations, residual 0, x = 0
+    op = G.KernelOperator(G.parse_kernel("(scale 1.3 (matern32 0.6))"), x, 0.2)
+    X, iters, res = op.cg(B, 1e-9, None)
+    assert iters[2] == 0 and res[2] == 0.0 and not X[:, 2].any()
+    for c in (0, 1, 3, 4):
+        one = G.cg_solve(op, np.ascontiguousarray(B[:, c]), G.CgConfig(rel_tolerance=1e-9))
+        assert abs(int(iters[c]) - one.iterations) <= 1
+        assert rel_l2(X[:, c], one.x) <= 1e-7
+    # non-convergence is reported, not raised
+    X, iters, res = op.cg(B[:, :1], 1e-14, 3)
+    assert iters[0] == 3 and res[0] > 0
+
+
+def test_slq_golden(gpu_ctx):
+    g = golden("slq_small.npz")
+    for ci in range(2):
+        n, d, seed, probes, steps, pseed = (int(a) for a in g[f"case_{ci}"])
+        x, _ = small_inputs(n, d, seed)
+        k = G.parse_kernel(str(g[f"tree_{ci}"]))
+        op = G.KernelOperator(k, x, 0.1)
+        ld = G.slq_logdet(op, n, G.CgConfig(probes=probes, lanczos_steps=steps), seed=pseed)
+        assert abs(ld - float(g[f"logdet_{ci}"])) <= 1e-4 * abs(float(g[f"logdet_{ci}"]))
+        z = G.probe_block(n, probes, pseed)
+        al, be, cnt = op.lanczos(z, min(steps, n))
+        for p in range(probes):
+            ra = g[f"alpha_{ci}_{p}"]
+            m = min(len(ra), int(cnt[p]), 8)  # leading coefficients agree closely
+            np.testing.assert_allclose(al[p, :m], ra[:m], rtol=1e-5)
+
+
+def test_model_cfg1_full(gpu_ctx):
+    g = golden("model_cfg1.npz")
+    cfg = O.CONFIGS["cfg1"]
+    x, y = O.synthetic(cfg["n"], cfg["d"])
+    k = G.parse_kernel(cfg["kernel"])
+    st = G.gp_fit(x, y, k, cfg["noise"], "cg")
+    assert abs(st.cg_iterations - int(g["it"])) <= 3
+    xs = np.linspace(0.0, 1.0, 101)[:, None]
+    mean, var = G.gp_predict(st, xs)
+    assert rel_l2(mean, g["mean"]) <= 1e-4
+    assert np.max(np.abs(var - g["var"])) <= 3e-3
+    assert np.max(np.abs(mean - g["chol_mean"])) <= 1e-4 * np.abs(g["chol_mean"]).max() + 1e-5
+    lml = G.log_marginal_likelihood(st, seed=0)
+    assert abs(lml - float(g["lml"])) <= 1e-4 * abs(float(g["lml"]))
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "model_small.npz")),
+                    reason="model_small fixture not generated")
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
+def test_model_small_matrix_free_branch(gpu_ctx, name):
+    g = golden("model_small.npz")
+    cfg = O.CONFIGS[name]
+    x, y = O.synthetic(3000, cfg["d"])
+    xs = np.random.default_rng(9).random((8, cfg["d"]))
+    st = G.gp_fit(x, y, G.parse_kernel(cfg["kernel"]), cfg["noise"], "cg")
+    it_ref = int(g[f"{name}_it"])
+    assert abs(st.cg_iterations - it_ref) <= max(3, 0.1 * it_ref)
+    mean, var = G.gp_predict(st, xs)
+    assert rel_l2(mean, g[f"{name}_mean"]) <= 1e-4
+    assert np.max(np.abs(var - g[f"{name}_var"])) <= 3e-3
+    lml = G.log_marginal_likelihood(st, seed=0)
+    assert abs(lml - float(g[f"{name}_lml"])) <= 1e-4 * abs(float(g[f"{name}_lml"]))
