@@ -104,3 +104,15 @@ def test_model_cfg1():
     np.testing.assert_array_equal(var, g["var"])
     lml = O.lml(nodes, x, y, cfg["noise"], alpha)
     assert lml == float(g["lml"])
+
+
+def test_model_small_fit_cfg4_kernel():
+    # matrix-free branch of gp_fit (N=3000 > 2048): the oracle reproduces the
+    # reference's CG iterates bit for bit
+    g = golden("model_small.npz")
+    cfg = O.CONFIGS["cfg4"]
+    x, y = O.synthetic(3000, cfg["d"])
+    assert digest(x) == str(g["cfg4_xsha"])
+    alpha, it, res = O.fit(O.parse_tree(cfg["kernel"]), x, y, cfg["noise"])
+    assert it == int(g["cfg4_it"])
+    np.testing.assert_array_equal(alpha, g["cfg4_alpha"])
