@@ -34,6 +34,7 @@ NODE_KINDS = {"rbf": 0, "matern12": 1, "matern32": 2, "matern52": 3, "periodic":
 DEVICE_PTRS = 1
 ACC_FP32 = 2
 DIST_DIRECT = 4
+FORCE_SIMT = 8
 
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)

@@ -49,3 +49,24 @@ struct LgpGramArgs {
 };
 
 #endif  // LGP_JIT_ABI_H_
+
+#ifndef LGP_TC_ABI_
+#define LGP_TC_ABI_
+// Tensor-core K1 (tcgen05, kind::tf32, 3xTF32): operands are pre-tiled in the
+// UMMA K-major no-swizzle canonical layout by the prep / pack kernels.
+struct LgpTcArgs {
+  const float* a1;      // row operand tiles   [n_rb][2 (hi,lo)][128 x KD]
+  const float* b1;      // column operand tiles [n_tiles][2][64 x KD]
+  const float* v;       // RHS tiles            [n_pass][n_tiles][2][TBN x 64]
+  double* partial;      // [n_seg][n_pass][n_rows_pad][TBN]
+  const int* done;      // optional early-exit flag
+  int n_rows_pad;
+  int n_rb;
+  int n_seg;
+  int n_pass;
+  int tiles_per_seg;
+  int n_tiles;
+  int pad_[2];
+  float kc[LGP_MAX_KC];
+};
+#endif

@@ -318,6 +318,12 @@ int lgp_kernel_jit(const lgp_kernel* k, int32_t d, int32_t t, uint32_t flags, ch
   Plan p = make_plan(k->tree, d, tb, flags);
   std::string lg;
   jit_compile(p.source, &lg);
+  Plan tp = make_tc_plan(k->tree, d, t, flags);
+  if (tp.tc) {
+    std::string lg2;
+    jit_compile(tp.source, &lg2);
+    lg += "\n[tensor-core module]\n" + lg2;
+  }
   if (log && cap) {
     const size_t n = std::min(cap - 1, lg.size());
     std::memcpy(log, lg.data(), n);
@@ -338,7 +344,8 @@ int lgp_kernel_source(const lgp_kernel* k, int32_t d, int32_t t, uint32_t flags,
   require(k && d >= 1 && t >= 1, LGP_E_ARG, "bad arguments");
   int tb = 1;
   while (tb < t && tb < 16) tb <<= 1;
-  Plan p = make_plan(k->tree, d, tb, flags);
+  Plan p = make_tc_plan(k->tree, d, t, flags);
+  if (!p.tc) p = make_plan(k->tree, d, tb, flags);
   if (needed) *needed = p.source.size() + 1;
   if (buf && cap) {
     const size_t n = std::min(cap - 1, p.source.size());
@@ -424,6 +431,7 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
     op.n_rows = r1 - r0;
     op.t = t;
     op.flags = flags;
+    op.allow_tc = true;
     op.tag = "api.mv";
     op.prepare();
     op.run(Vd, od + r0 * t, square ? noise : 0.0, square ? Vd + r0 * t : nullptr, nullptr);

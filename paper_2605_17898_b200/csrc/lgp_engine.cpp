@@ -55,15 +55,21 @@ void launch(Context* ctx, CUfunction f, unsigned gx, unsigned gy, unsigned bx, s
 }  // namespace
 
 void MatvecOp::prepare() {
-  const int tb = pick_tb(t);
-  plan = make_plan(k->tree, rows->d, tb, flags);
+  int tb = pick_tb(t);
+  if (allow_tc) plan = make_tc_plan(k->tree, rows->d, t, flags);
+  if (plan.tc) {
+    tb = plan.tc_n;
+  } else {
+    plan = make_plan(k->tree, rows->d, tb, flags);
+  }
   mod = get_module(ctx, plan);
   const Tuning& tu = plan.tune;
-  const int rows_per_cta = tu.threads * tu.r;
+  const int rows_per_cta = plan.tc ? 128 : tu.threads * tu.r;
   n_rb = (int)ceil_div<int64_t>(std::max<int64_t>(n_rows, 1), rows_per_cta);
   n_rows_pad = n_rb * rows_per_cta;
-  n_tiles = (int)ceil_div<int64_t>(std::max<int64_t>(cols->n, 1), tu.cc);
-  n_cols_pad = n_tiles * tu.cc;
+  const int cc = plan.tc ? 64 : tu.cc;
+  n_tiles = (int)ceil_div<int64_t>(std::max<int64_t>(cols->n, 1), cc);
+  n_cols_pad = n_tiles * cc;
   n_pass = ceil_div(t, tb);
 
   // Column split so that (row blocks x segments x passes) CTAs fill whole
@@ -84,10 +90,43 @@ void MatvecOp::prepare() {
   tiles_per_seg = ceil_div(n_tiles, best);
   n_seg = ceil_div(n_tiles, tiles_per_seg);
 
+  partial = (double*)ctx->scratch_get(tag + ".part", (size_t)n_seg * n_pass * n_rows_pad * tb * 8);
+  if (plan.tc) {
+    // operands pre-tiled in the UMMA canonical layout, TF32 hi/lo split
+    fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * 2 * plan.tc_kd * 4);
+    fc = (float*)ctx->scratch_get(tag + ".b1", (size_t)n_cols_pad * 2 * plan.tc_kd * 4);
+    vtc = (float*)ctx->scratch_get(tag + ".vtc", (size_t)n_pass * n_cols_pad * 2 * tb * 4);
+    LgpPrepArgs pa = plan.prep;
+    pa.x = rows->x;
+    pa.ctr = cols->ctr;
+    pa.fr = fr;
+    pa.fc = fc;
+    pa.row0 = row0;
+    pa.n = n_rows;
+    pa.n_pad = n_rows_pad;
+    int tile_rows = 128, is_col = 0;
+    void* p1[] = {&pa, &tile_rows, &is_col};
+    LGP_CU_CHECK(drv::LaunchKernel(mod->prep, (unsigned)ceil_div<int64_t>(n_rows_pad, 128), 1, 1,
+                                   128, 1, 1, 0, (CUstream)ctx->stream, p1, nullptr));
+    ++ctx->launches;
+    LgpPrepArgs pc = plan.prep;
+    pc.x = cols->x;
+    pc.ctr = cols->ctr;
+    pc.fr = fr;
+    pc.fc = fc;
+    pc.row0 = 0;
+    pc.n = cols->n;
+    pc.n_pad = n_cols_pad;
+    int tile_cols = 64, is_col1 = 1;
+    void* p2[] = {&pc, &tile_cols, &is_col1};
+    LGP_CU_CHECK(drv::LaunchKernel(mod->prep, (unsigned)ceil_div<int64_t>(n_cols_pad, 128), 1, 1,
+                                   128, 1, 1, 0, (CUstream)ctx->stream, p2, nullptr));
+    ++ctx->launches;
+    return;
+  }
   fr = (float*)ctx->scratch_get(tag + ".fr", (size_t)n_rows_pad * plan.fr * 4);
   fc = (float*)ctx->scratch_get(tag + ".fc", (size_t)n_cols_pad * plan.fc * 4);
   vpack = (double*)ctx->scratch_get(tag + ".v", (size_t)n_pass * n_cols_pad * tb * 8);
-  partial = (double*)ctx->scratch_get(tag + ".part", (size_t)n_seg * n_pass * n_rows_pad * tb * 8);
 
   // features of the local rows and of all columns, centred on the column set
   LgpPrepArgs pa = plan.prep;
@@ -113,6 +152,46 @@ void MatvecOp::prepare() {
 void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const double* noise_v,
                    const int* done) {
   const int tb = plan.tune.tb;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  auto prof_begin = [&]() {
+    if (!ctx->profile) return;
+    if (ctx->ev_pool.empty()) {
+      LGP_CUDA_CHECK(cudaEventCreate(&ev.first));
+      LGP_CUDA_CHECK(cudaEventCreate(&ev.second));
+    } else {
+      ev = ctx->ev_pool.back();
+      ctx->ev_pool.pop_back();
+    }
+    LGP_CUDA_CHECK(cudaEventRecord(ev.first, ctx->stream));
+  };
+  auto prof_end = [&]() {
+    if (!ctx->profile) return;
+    LGP_CUDA_CHECK(cudaEventRecord(ev.second, ctx->stream));
+    ctx->ev_pending.push_back(ev);
+  };
+  if (plan.tc) {
+    vec::pack_rhs_tc(ctx, V_dev, cols->n, t, n_tiles, tb, n_pass, vtc, done);
+    LgpTcArgs a = plan.tca;
+    a.a1 = fr;
+    a.b1 = fc;
+    a.v = vtc;
+    a.partial = partial;
+    a.done = done;
+    a.n_rows_pad = n_rows_pad;
+    a.n_rb = n_rb;
+    a.n_seg = n_seg;
+    a.n_pass = n_pass;
+    a.tiles_per_seg = tiles_per_seg;
+    a.n_tiles = n_tiles;
+    const int64_t grid = (int64_t)n_rb * n_seg * n_pass;
+    if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
+    prof_begin();
+    launch(ctx, mod->matvec, (unsigned)grid, 1, 320, plan.smem_bytes, &a);
+    prof_end();
+    vec::epilogue(ctx, partial, n_seg, n_pass, n_rows_pad, tb, n_rows, t, plan.root_scale, noise,
+                  noise_v, out_dev, done);
+    return;
+  }
   vec::pack_rhs(ctx, V_dev, cols->n, t, n_cols_pad, tb, n_pass, vpack, done);
   LgpMatvecArgs a = plan.mv;
   a.fr = fr;
@@ -129,22 +208,9 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
   a.n_tiles = n_tiles;
   const int64_t grid = (int64_t)n_rb * n_seg * n_pass;
   if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
-  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-  if (ctx->profile) {
-    if (ctx->ev_pool.empty()) {
-      LGP_CUDA_CHECK(cudaEventCreate(&ev.first));
-      LGP_CUDA_CHECK(cudaEventCreate(&ev.second));
-    } else {
-      ev = ctx->ev_pool.back();
-      ctx->ev_pool.pop_back();
-    }
-    LGP_CUDA_CHECK(cudaEventRecord(ev.first, ctx->stream));
-  }
+  prof_begin();
   launch(ctx, mod->matvec, (unsigned)grid, 1, plan.tune.threads, plan.smem_bytes, &a);
-  if (ctx->profile) {
-    LGP_CUDA_CHECK(cudaEventRecord(ev.second, ctx->stream));
-    ctx->ev_pending.push_back(ev);
-  }
+  prof_end();
   vec::epilogue(ctx, partial, n_seg, n_pass, n_rows_pad, tb, n_rows, t, plan.root_scale, noise,
                 noise_v, out_dev, done);
 }
@@ -282,6 +348,7 @@ void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, doub
   op.row0 = r0;
   op.n_rows = r1 - r0;
   op.t = t;
+  op.allow_tc = true;
   op.tag = "lz.mv";
   op.prepare();
 

@@ -95,14 +95,23 @@ struct Plan {
   LgpMatvecArgs mv{};       // kc[] filled
   LgpGramArgs gram{};       // pc[] filled (includes the root scale)
   size_t smem_bytes = 0;
+  // tensor-core variant (tcgen05 3xTF32): r^2-stationary trees, D >= 4, t >= 8
+  bool tc = false;
+  int tc_kd = 0;            // K of the distance GEMM (D + 2, multiple of 8)
+  int tc_n = 16;            // RHS per pass (GEMM2 N)
+  LgpTcArgs tca{};          // kc[] filled
 };
 
 Plan make_plan(const Tree& tree, int d, int tb, uint32_t flags);
+// The tensor-core plan for the same tree, or a plan with tc == false when the
+// tree / shape is not eligible (see lgp_codegen.cpp).
+Plan make_tc_plan(const Tree& tree, int d, int t, uint32_t flags);
 
 // A loaded JIT module.
 struct Module {
   CUmodule mod = nullptr;
   CUfunction prep = nullptr, matvec = nullptr, gram = nullptr, diag = nullptr;
+  bool tc = false;  // module holds lgp_tc_prep / lgp_matvec_tc in prep / matvec
   int blocks_per_sm = 1;
   int regs = 0;
   std::string log;
@@ -182,9 +191,11 @@ struct MatvecOp {
   // prepared state
   Plan plan;
   Module* mod = nullptr;
+  bool allow_tc = false;  // may use the tensor-core K1 (matvec API, Lanczos; not CG)
   float* fr = nullptr;
   float* fc = nullptr;
   double* vpack = nullptr;
+  float* vtc = nullptr;
   double* partial = nullptr;
   int n_rows_pad = 0, n_cols_pad = 0, n_rb = 0, n_seg = 0, n_pass = 0, n_tiles = 0,
       tiles_per_seg = 0;
@@ -209,6 +220,10 @@ namespace vec {
 int reduce_blocks(int64_t n, int t);
 void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int tb, int n_pass,
               double* out, const int* done);
+// RHS tiles for the tensor-core K1: [n_pass][n_tiles][hi,lo][tbn x 64] TF32 split,
+// UMMA K-major canonical layout
+void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int tbn, int n_pass,
+                 float* out, const int* done);
 void epilogue(Context* c, const double* partial, int n_seg, int n_pass, int64_t rows_pad, int tb,
               int64_t n_rows, int t, double scale, double noise, const double* noise_v,
               double* out, const int* done);

@@ -127,7 +127,10 @@ std::string jit_compile(const std::string& source, std::string* log_out) {
   const std::string path = dir.empty() ? "" : dir + "/" + hex + ".cubin";
   std::string cubin;
   if (!path.empty() && read_file(path, cubin)) {
-    if (log_out) read_file(dir + "/" + hex + ".log", *log_out);
+    if (log_out) {
+      read_file(dir + "/" + hex + ".log", *log_out);
+      while (!log_out->empty() && log_out->back() == '\0') log_out->pop_back();
+    }
     return cubin;
   }
   nvrtcProgram prog;
@@ -139,6 +142,7 @@ std::string jit_compile(const std::string& source, std::string* log_out) {
   nvrtc().GetProgramLogSize(prog, &logn);
   std::string log(logn, '\0');
   if (logn) nvrtc().GetProgramLog(prog, &log[0]);
+  while (!log.empty() && log.back() == '\0') log.pop_back();
   if (rc != NVRTC_SUCCESS) {
     nvrtc().DestroyProgram(&prog);
     throw Error(LGP_E_COMPILE, std::string("NVRTC: ") + nvrtc().GetErrorString(rc) + "\n" + log);
@@ -163,10 +167,16 @@ Module* get_module(Context* ctx, const Plan& plan) {
   std::unique_ptr<Module> m(new Module);
   const std::string cubin = jit_compile(plan.source, &m->log);
   LGP_CU_CHECK(drv::ModuleLoadData(&m->mod, cubin.data()));
-  LGP_CU_CHECK(drv::ModuleGetFunction(&m->prep, m->mod, "lgp_prep"));
-  LGP_CU_CHECK(drv::ModuleGetFunction(&m->matvec, m->mod, "lgp_matvec"));
-  LGP_CU_CHECK(drv::ModuleGetFunction(&m->gram, m->mod, "lgp_gram"));
-  LGP_CU_CHECK(drv::ModuleGetFunction(&m->diag, m->mod, "lgp_diag"));
+  m->tc = plan.tc;
+  if (plan.tc) {
+    LGP_CU_CHECK(drv::ModuleGetFunction(&m->prep, m->mod, "lgp_tc_prep"));
+    LGP_CU_CHECK(drv::ModuleGetFunction(&m->matvec, m->mod, "lgp_matvec_tc"));
+  } else {
+    LGP_CU_CHECK(drv::ModuleGetFunction(&m->prep, m->mod, "lgp_prep"));
+    LGP_CU_CHECK(drv::ModuleGetFunction(&m->matvec, m->mod, "lgp_matvec"));
+    LGP_CU_CHECK(drv::ModuleGetFunction(&m->gram, m->mod, "lgp_gram"));
+    LGP_CU_CHECK(drv::ModuleGetFunction(&m->diag, m->mod, "lgp_diag"));
+  }
   LGP_CU_CHECK(drv::FuncSetAttribute(m->matvec, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                                   (int)plan.smem_bytes));
   LGP_CU_CHECK(drv::FuncGetAttribute(&m->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, m->matvec));

@@ -81,6 +81,32 @@ __global__ void k_pack(const double* __restrict__ V, long long n, int t, long lo
   }
 }
 
+__global__ void k_pack_tc(const double* __restrict__ V, long long n, int t, int n_tiles, int tbn,
+                          int n_pass, float* __restrict__ out, const int* done) {
+  if (is_done(done)) return;
+  const long long total = (long long)n_pass * n_tiles * tbn * 64;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int jj = (int)(e & 63);
+    const int c = (int)((e >> 6) % tbn);
+    const long long pt = (e >> 6) / tbn;  // pass * n_tiles + tile
+    const long long tile = pt % n_tiles;
+    const int pass = (int)(pt / n_tiles);
+    const long long j = tile * 64 + jj;
+    const int col = pass * tbn + c;
+    const double v = (j < n && col < t) ? V[j * t + col] : 0.0;
+    const float f = (float)v;
+    const float hi = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
+    const float lo = (float)(v - (double)hi);
+    // K-major canonical tile (rows = RHS c, K = column jj): 8-row groups of
+    // 16 x 128 B, K halves 128 B apart
+    const int off = (c >> 3) * 512 + (jj >> 2) * 32 + (c & 7) * 4 + (jj & 3);
+    float* base = out + pt * 2 * tbn * 64;
+    base[off] = hi;
+    base[tbn * 64 + off] = lo;
+  }
+}
+
 __global__ void k_epilogue(const double* __restrict__ partial, int n_seg, int n_pass,
                            long long rows_pad, int tb, long long n_rows, int t, double scale,
                            double noise, const double* __restrict__ noise_v,
@@ -391,6 +417,13 @@ void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int 
               double* out, const int* done) {
   k_pack<<<grid_for((long long)n_pass * n_pad * tb), 256, 0, c->stream>>>(V, n, t, n_pad, tb,
                                                                          n_pass, out, done);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int tbn, int n_pass,
+                 float* out, const int* done) {
+  k_pack_tc<<<grid_for((long long)n_pass * n_tiles * tbn * 64), 256, 0, c->stream>>>(
+      V, n, t, n_tiles, tbn, n_pass, out, done);
   LGP_LAUNCH_CHECK(c);
 }
 
