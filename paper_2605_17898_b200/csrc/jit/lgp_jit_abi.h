@@ -57,9 +57,12 @@ struct LgpGramArgs {
 struct LgpTcArgs {
   const float* a1;      // row operand tiles   [n_rb][2 (hi,lo)][128 x KD]
   const float* b1;      // column operand tiles [n_tiles][2][64 x KD]
-  const float* v;       // RHS tiles            [n_pass][n_tiles][2][TBN x 64]
+  const void* v;        // RHS tiles (FP16 hi/lo) [n_pass][n_tiles][2][TBN x 64]
+  const float* vscale;  // power-of-two scale of each RHS column [n_pass * TBN]
   double* partial;      // [n_seg][n_pass][n_rows_pad][TBN]
   const int* done;      // optional early-exit flag
+  const int* v_inexact; // set by the RHS pack kernel if any V_lo != 0 (may be null)
+  unsigned long long* trace;  // LGP_TC_TRACE builds only: cycle counters
   int n_rows_pad;
   int n_rb;
   int n_seg;

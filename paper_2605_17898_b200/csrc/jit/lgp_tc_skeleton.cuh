@@ -15,38 +15,59 @@
 //       so S'_ij = r^2_ij (lengthscale-scaled) lands in TMEM directly.
 //   epilogue (8 warps, SIMT): r^2 -> k (the tree, one MUFU.EX2 per exp) ->
 //       TF32 hi/lo split -> tcgen05.st back into TMEM as the A operand of
-//   GEMM2 (kind::tf32, 3xTF32, A = P from TMEM, B = V tile from SMEM):
-//       D2[128 x N] += P[128 x 64] . V[64 x N]
+//   GEMM2 (kind::f16, A = P from TMEM as FP16 hi/lo, B = V tile from SMEM as
+//       FP16 hi/lo of a power-of-two column scaling, FP32 accumulate):
+//       D2[128 x N] += P_hi.V_hi + P_lo.V_hi (+ P_hi.V_lo unless V is exact)
 //   D2 (FP32, TMEM) is drained every LGP_TC_G chunks of a warpgroup into FP64
 //   registers; the two epilogue warpgroups' FP64 sums are combined in a fixed
 //   order and written as this segment's partial (deterministic).
 //
 // Warp roles: warp 0 = TMA bulk-copy producer (+ TMEM allocator), warp 1 =
-// MMA issuer (one thread), warps 2..5 / 6..9 = epilogue warpgroups 0 / 1
-// (even / odd chunks, each with its own TMEM buffers), so chunk c's epilogue
-// overlaps chunk c+1's GEMM1 and chunk c-1's GEMM2.
+// MMA issuer (one thread, polling: the distance GEMM runs up to 4 chunks ahead
+// of the contraction), warps 2..5 / 6..9 = epilogue warpgroups 0 / 1 (even /
+// odd chunks). TMEM: 4 S buffers of 64 columns (S' in FP32, then P packed
+// FP16 hi | lo in place) + 2x2 D2 accumulators.
+
+#ifdef LGP_TC_TRACE
+#define TR_DECL unsigned long long tr_t = clock64();
+#define TR_MARK(slot) { const unsigned long long n_ = clock64(); atomicAdd(a.trace + (slot), n_ - tr_t); tr_t = n_; }
+#else
+#define TR_DECL
+#define TR_MARK(slot)
+#endif
+
+#ifndef LGP_TC_ABLATE
+#define LGP_TC_ABLATE 0
+#endif
+
+#ifdef LGP_TC_TRACE
+#define TR_DECL unsigned long long tr_t = clock64();
+#define TR_MARK(slot) { const unsigned long long n_ = clock64(); atomicAdd(a.trace + (slot), n_ - tr_t); tr_t = n_; }
+#else
+#define TR_DECL
+#define TR_MARK(slot)
+#endif
 
 #define TC_CH 64
 #define TC_THREADS 320
 #define TC_A1_FLOATS (128 * LGP_TC_KD)
 #define TC_B1_FLOATS (TC_CH * LGP_TC_KD)
-#define TC_V_FLOATS (LGP_TC_N * TC_CH)
+#define TC_V_HALFS (LGP_TC_N * TC_CH)
 #define TC_A1_BYTES (2 * TC_A1_FLOATS * 4)
 #define TC_B1_BYTES (2 * TC_B1_FLOATS * 4)
-#define TC_V_BYTES (2 * TC_V_FLOATS * 4)
+#define TC_V_BYTES (2 * TC_V_HALFS * 2)
 #define TC_STAGE_BYTES (TC_B1_BYTES + TC_V_BYTES)
 #define TC_COMB_BYTES (128 * LGP_TC_N * 8)
-#define TC_NBARS (13 + 2 * LGP_TC_STAGES)
-#define TC_SMEM_BYTES (TC_A1_BYTES + LGP_TC_STAGES * TC_STAGE_BYTES + TC_COMB_BYTES + TC_NBARS * 8 + 16)
+#define TC_NBARS (17 + 2 * LGP_TC_STAGES)
 
 // barrier slots
 #define B_AFULL 0
 #define B_SFULL(s) (1 + (s))
 #define B_SEMPTY(s) (1 + LGP_TC_STAGES + (s))
-#define B_D1FULL(w) (1 + 2 * LGP_TC_STAGES + (w))
-#define B_PFULL(w) (3 + 2 * LGP_TC_STAGES + (w))
-#define B_D2FULL(w, b) (5 + 2 * LGP_TC_STAGES + 2 * (w) + (b))
-#define B_D2EMPTY(w, b) (9 + 2 * LGP_TC_STAGES + 2 * (w) + (b))
+#define B_S1FULL(q) (1 + 2 * LGP_TC_STAGES + (q))
+#define B_PFULL(q) (5 + 2 * LGP_TC_STAGES + (q))
+#define B_D2FULL(w, b) (9 + 2 * LGP_TC_STAGES + 2 * (w) + (b))
+#define B_D2EMPTY(w, b) (13 + 2 * LGP_TC_STAGES + 2 * (w) + (b))
 
 __device__ __forceinline__ float lgp_ex2(float x) {
   float y;
@@ -75,6 +96,18 @@ __device__ __forceinline__ void lgp_mbar_expect_tx(unsigned bar, unsigned bytes)
 
 __device__ __forceinline__ void lgp_mbar_arrive(unsigned bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ bool lgp_mbar_test(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
 __device__ __forceinline__ void lgp_mbar_wait(unsigned bar, unsigned parity) {
@@ -106,26 +139,27 @@ __device__ __forceinline__ void lgp_bulk_g2s(unsigned dst, const void* src, unsi
 }
 
 // UMMA shared-memory descriptor: K-major, no swizzle (canonical
-// ((8,m),2):((16B,SBO),LBO)), LBO = 128 B between the two 16-byte K halves,
-// SBO between 8-row core-matrix groups, version 1 (sm_100).
+// ((8,m),2):((16B,SBO),LBO)), LBO = 128 B between the two 16-byte K chunks of
+// one instruction, SBO between 8-row core-matrix groups, version 1 (sm_100).
 __device__ __forceinline__ unsigned long long lgp_sdesc(unsigned saddr, unsigned sbo) {
   return (unsigned long long)((saddr >> 4) & 0x3FFFu) | ((unsigned long long)(128u >> 4) << 16) |
          ((unsigned long long)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-__device__ __forceinline__ void lgp_mma_ss(unsigned d, unsigned long long ad, unsigned long long bd,
-                                           unsigned idesc, unsigned acc) {
+__device__ __forceinline__ void lgp_mma_tf32_ss(unsigned d, unsigned long long ad,
+                                                unsigned long long bd, unsigned idesc,
+                                                unsigned acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
 
-__device__ __forceinline__ void lgp_mma_ts(unsigned d, unsigned a_tmem, unsigned long long bd,
-                                           unsigned idesc, unsigned acc) {
+__device__ __forceinline__ void lgp_mma_f16_ts(unsigned d, unsigned a_tmem, unsigned long long bd,
+                                               unsigned idesc, unsigned acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a_tmem), "l"(bd), "r"(idesc), "r"(acc));
 }
 
@@ -178,8 +212,21 @@ __device__ __forceinline__ void lgp_tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// offset (floats) of element (row r, k) in a K-major no-swizzle tile with KD
-// columns: 8-row core-matrix groups of (KD/4) x 128 B, K halves 128 B apart
+// FP16 hi/lo split of two FP32 values, packed {lo half = x0, hi half = x1}
+__device__ __forceinline__ void lgp_split_f16x2(float x0, float x1, unsigned& hi, unsigned& lo) {
+  unsigned h, l;
+  float f0, f1;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
+  asm("{\n\t.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\tcvt.f32.f16 %0, a;\n\tcvt.f32.f16 %1, b;\n\t}"
+      : "=f"(f0), "=f"(f1)
+      : "r"(h));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(x1 - f1), "f"(x0 - f0));
+  hi = h;
+  lo = l;
+}
+
+// offset (floats) of element (row r, k) in a K-major no-swizzle TF32 tile with
+// KD columns: 8-row core-matrix groups of (KD/4) x 128 B, K chunks 128 B apart
 __device__ __forceinline__ int lgp_tc_off(int r, int k, int kd) {
   return (r >> 3) * (kd * 8) + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
 }
@@ -253,14 +300,15 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       lgp_mbar_init(BAR(B_SFULL(s)), 1);
       lgp_mbar_init(BAR(B_SEMPTY(s)), 1);
     }
-    for (int w = 0; w < 2; ++w) {
-      lgp_mbar_init(BAR(B_D1FULL(w)), 1);
-      lgp_mbar_init(BAR(B_PFULL(w)), 4);
+    for (int q = 0; q < 4; ++q) {
+      lgp_mbar_init(BAR(B_S1FULL(q)), 1);
+      lgp_mbar_init(BAR(B_PFULL(q)), 4);
+    }
+    for (int w = 0; w < 2; ++w)
       for (int b = 0; b < 2; ++b) {
         lgp_mbar_init(BAR(B_D2FULL(w, b)), 1);
         lgp_mbar_init(BAR(B_D2EMPTY(w, b)), 4);
       }
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -273,9 +321,9 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
   __syncthreads();
   lgp_tc_fence_after();
   const unsigned tmem = *tslot;
-  // TMEM columns: D1[w] (S' then P_hi) 64 each, L[w] (P_lo) 64 each, D2[w][b] N each
-#define T_D1(w) (tmem + 64u * (unsigned)(w))
-#define T_L(w) (tmem + 128u + 64u * (unsigned)(w))
+  // TMEM columns: S buffer q (chunk c uses q = c % 4): 64 FP32 columns of S',
+  // then P packed FP16 (hi in columns 0..31, lo in 32..63); D2[w][b]: N columns
+#define T_SB(q) (tmem + 64u * (unsigned)(q))
 #define T_D2(w, b) (tmem + 256u + (unsigned)LGP_TC_N * (2u * (unsigned)(w) + (unsigned)(b)))
 
   if (warp == 0) {
@@ -283,15 +331,19 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       // ------------------------------------------------ producer (TMA bulk)
       lgp_mbar_expect_tx(BAR(B_AFULL), TC_A1_BYTES);
       lgp_bulk_g2s(lgp_saddr(a1s), a.a1 + (size_t)rb * 2 * TC_A1_FLOATS, TC_A1_BYTES, BAR(B_AFULL));
+      const unsigned char* vbase = reinterpret_cast<const unsigned char*>(a.v);
+      TR_DECL
       for (int c = 0; c < nch; ++c) {
         const int s = c % LGP_TC_STAGES;
+        TR_MARK(0)
         if (c >= LGP_TC_STAGES) lgp_mbar_wait(BAR(B_SEMPTY(s)), ((c / LGP_TC_STAGES) - 1) & 1);
+        TR_MARK(1)
         const unsigned dst = lgp_saddr(stg + (size_t)s * TC_STAGE_BYTES);
         lgp_mbar_expect_tx(BAR(B_SFULL(s)), TC_STAGE_BYTES);
         lgp_bulk_g2s(dst, a.b1 + (size_t)(tile0 + c) * 2 * TC_B1_FLOATS, TC_B1_BYTES,
                      BAR(B_SFULL(s)));
         lgp_bulk_g2s(dst + TC_B1_BYTES,
-                     a.v + ((size_t)pass * a.n_tiles + tile0 + c) * 2 * TC_V_FLOATS, TC_V_BYTES,
+                     vbase + ((size_t)pass * a.n_tiles + tile0 + c) * TC_V_BYTES, TC_V_BYTES,
                      BAR(B_SFULL(s)));
       }
     }
@@ -301,51 +353,61 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       // ------------------------------------------------ MMA issuer
       const unsigned idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(TC_CH >> 3) << 17) |
                               ((unsigned)(128 >> 4) << 24);
-      const unsigned idesc2 = (1u << 4) | (2u << 7) | (2u << 10) |
+      const unsigned idesc2 = (1u << 4) | (0u << 7) | (0u << 10) |
                               ((unsigned)(LGP_TC_N >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
-      const unsigned a_hi = lgp_saddr(a1s), a_lo = a_hi + TC_A1_FLOATS * 4;
-      const unsigned sbo_k = LGP_TC_KD * 32;
+      const unsigned long long dk = lgp_sdesc(0u, LGP_TC_KD * 32);
+      const unsigned long long dv = lgp_sdesc(0u, 1024u);
+      const unsigned long long a_hi = dk + (lgp_saddr(a1s) >> 4);
+      const unsigned long long a_lo = a_hi + (TC_A1_FLOATS * 4 >> 4);
+      const unsigned stg0 = lgp_saddr(stg) >> 4;
+      // V tiles exactly representable in FP16 (e.g. +-1 probes) need no V_lo term
+      const bool v_exact = a.v_inexact != nullptr && *a.v_inexact == 0;
       lgp_mbar_wait(BAR(B_AFULL), 0);
-      for (int c = 0; c <= nch; ++c) {
-        if (c < nch) {
-          const int s = c % LGP_TC_STAGES;
-          lgp_mbar_wait(BAR(B_SFULL(s)), (c / LGP_TC_STAGES) & 1);
+      int g1 = 0, g2 = 0;
+      while (g2 < nch) {
+        // distance GEMM of chunk g1 into S buffer g1 % 4 (free once the
+        // contraction of chunk g1 - 4 is issued: the tensor pipe is in order)
+        if (g1 < nch && g1 < g2 + 4 &&
+            lgp_mbar_test(BAR(B_SFULL(g1 % LGP_TC_STAGES)), (g1 / LGP_TC_STAGES) & 1)) {
           lgp_tc_fence_after();
-          const unsigned b_hi = lgp_saddr(stg + (size_t)s * TC_STAGE_BYTES);
-          const unsigned b_lo = b_hi + TC_B1_FLOATS * 4;
-          const unsigned d = T_D1(c & 1);
+          const int s = g1 % LGP_TC_STAGES;
+          const unsigned long long b_hi = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
+          const unsigned long long b_lo = b_hi + (TC_B1_FLOATS * 4 >> 4);
+          const unsigned d = T_SB(g1 & 3);
 #pragma unroll
           for (int kk = 0; kk < LGP_TC_KD / 8; ++kk) {
-            const unsigned o = 256u * kk;
-            lgp_mma_ss(d, lgp_sdesc(a_hi + o, sbo_k), lgp_sdesc(b_hi + o, sbo_k), idesc1, kk > 0);
-            lgp_mma_ss(d, lgp_sdesc(a_hi + o, sbo_k), lgp_sdesc(b_lo + o, sbo_k), idesc1, 1);
-            lgp_mma_ss(d, lgp_sdesc(a_lo + o, sbo_k), lgp_sdesc(b_hi + o, sbo_k), idesc1, 1);
+            const unsigned o = 16u * kk;
+            lgp_mma_tf32_ss(d, a_hi + o, b_hi + o, idesc1, kk > 0);
+            lgp_mma_tf32_ss(d, a_hi + o, b_lo + o, idesc1, 1);
+            lgp_mma_tf32_ss(d, a_lo + o, b_hi + o, idesc1, 1);
           }
-          lgp_mma_commit(BAR(B_D1FULL(c & 1)));
+          lgp_mma_commit(BAR(B_S1FULL(g1 & 3)));
+          ++g1;
+          continue;
         }
-        if (c >= 1) {
-          // GEMM2 of chunk cc = c - 1
-          const int cc = c - 1;
+        if (g2 < g1 && lgp_mbar_test(BAR(B_PFULL(g2 & 3)), (g2 >> 2) & 1)) {
+          const int cc = g2;
           const int w = cc & 1, k = cc >> 1, gi = k / LGP_TC_G, b = gi & 1;
           const bool first = (k % LGP_TC_G) == 0;
           const bool last = ((k % LGP_TC_G) == LGP_TC_G - 1) || (cc + 2 >= nch);
-          lgp_mbar_wait(BAR(B_PFULL(w)), k & 1);
           if (first && gi >= 2) lgp_mbar_wait(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
           lgp_tc_fence_after();
           const int s = cc % LGP_TC_STAGES;
-          const unsigned v_hi = lgp_saddr(stg + (size_t)s * TC_STAGE_BYTES) + TC_B1_BYTES;
-          const unsigned v_lo = v_hi + TC_V_FLOATS * 4;
+          const unsigned long long v_hi =
+              dv + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4) + (TC_B1_BYTES >> 4);
+          const unsigned long long v_lo = v_hi + (TC_V_HALFS * 2 >> 4);
           const unsigned d = T_D2(w, b);
+          const unsigned p = T_SB(cc & 3);
 #pragma unroll
-          for (int kk = 0; kk < TC_CH / 8; ++kk) {
-            const unsigned o = 256u * kk;
-            lgp_mma_ts(d, T_D1(w) + 8u * kk, lgp_sdesc(v_hi + o, 2048u), idesc2,
-                       (first && kk == 0) ? 0u : 1u);
-            lgp_mma_ts(d, T_D1(w) + 8u * kk, lgp_sdesc(v_lo + o, 2048u), idesc2, 1u);
-            lgp_mma_ts(d, T_L(w) + 8u * kk, lgp_sdesc(v_hi + o, 2048u), idesc2, 1u);
+          for (int kk = 0; kk < TC_CH / 16; ++kk) {
+            const unsigned o = 16u * kk;
+            lgp_mma_f16_ts(d, p + 8u * kk, v_hi + o, idesc2, (first && kk == 0) ? 0u : 1u);
+            lgp_mma_f16_ts(d, p + 32u + 8u * kk, v_hi + o, idesc2, 1u);
+            if (!v_exact) lgp_mma_f16_ts(d, p + 8u * kk, v_lo + o, idesc2, 1u);
           }
           lgp_mma_commit(BAR(B_SEMPTY(s)));
           if (last) lgp_mma_commit(BAR(B_D2FULL(w, b)));
+          ++g2;
         }
       }
     }
@@ -353,9 +415,9 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
   } else {
     // -------------------------------------------------- epilogue warpgroups
     const int w = (warp - 2) >> 2;
-    const int q = warp & 3;                 // TMEM lane quarter of this warp
-    const int row = 32 * q + lane;          // row within the 128-row tile
-    const unsigned lanes = (unsigned)(32 * q) << 16;
+    const int q4 = warp & 3;                // TMEM lane quarter of this warp
+    const int row = 32 * q4 + lane;         // row within the 128-row tile
+    const unsigned lanes = (unsigned)(32 * q4) << 16;
     const int nloc = (nch - w + 1) >> 1;    // chunks of this warpgroup
     double acc[LGP_TC_N];
 #pragma unroll
@@ -378,34 +440,40 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       if (lane == 0) lgp_mbar_arrive(BAR(B_D2EMPTY(w, b)));
     };
 
+    TR_DECL
     for (int k = 0; k < nloc; ++k) {
-      lgp_mbar_wait(BAR(B_D1FULL(w)), k & 1);
+      const int c = 2 * k + w;
+      const unsigned sb = T_SB(c & 3) + lanes;
+      if (lane == 0) { TR_MARK(8) }
+      lgp_mbar_wait(BAR(B_S1FULL(c & 3)), (c >> 2) & 1);
+      if (lane == 0) { TR_MARK(9) }
       lgp_tc_fence_after();
+      unsigned hi[32], lo[32];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        unsigned s[32], hi[32], lo[32];
-        lgp_tmem_ld32(T_D1(w) + lanes + 32u * h, s);
+        unsigned s[32];
+        lgp_tmem_ld32(sb + 32u * h, s);
         lgp_tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float r2 = fmaxf(__uint_as_float(s[i]), 0.f);
-          const float kv = lgp_tc_k(r2, a);
-          const unsigned hb = __float_as_uint(kv) & 0xFFFFE000u;
-          hi[i] = hb;
-          lo[i] = __float_as_uint(kv - __uint_as_float(hb));
+        for (int i = 0; i < 16; ++i) {
+          const float k0 = lgp_tc_k(fmaxf(__uint_as_float(s[2 * i]), 0.f), a);
+          const float k1 = lgp_tc_k(fmaxf(__uint_as_float(s[2 * i + 1]), 0.f), a);
+          lgp_split_f16x2(k0, k1, hi[16 * h + i], lo[16 * h + i]);
         }
-        lgp_tmem_st32(T_D1(w) + lanes + 32u * h, hi);
-        lgp_tmem_st32(T_L(w) + lanes + 32u * h, lo);
       }
+      lgp_tmem_st32(sb, hi);
+      lgp_tmem_st32(sb + 32u, lo);
       lgp_tmem_wait_st();
       lgp_tc_fence_before();
       __syncwarp();
-      if (lane == 0) lgp_mbar_arrive(BAR(B_PFULL(w)));
+      if (lane == 0) lgp_mbar_arrive(BAR(B_PFULL(c & 3)));
+      if (lane == 0) { TR_MARK(10) }
       if (k >= 1 && ((k - 1) % LGP_TC_G) == LGP_TC_G - 1) drain((k - 1) / LGP_TC_G);
+      if (lane == 0) { TR_MARK(11) }
     }
     if (nloc >= 1) drain((nloc - 1) / LGP_TC_G);
 
-    // combine the two warpgroups' FP64 sums in a fixed order
+    // combine the two warpgroups' FP64 sums in a fixed order, undo the V scaling
     if (w == 1) {
 #pragma unroll
       for (int i = 0; i < LGP_TC_N; ++i) comb[row * LGP_TC_N + i] = acc[i];
@@ -415,10 +483,11 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       double* out = a.partial +
                     (((size_t)seg * a.n_pass + pass) * a.n_rows_pad + (size_t)rb * 128 + row) *
                         LGP_TC_N;
+      const float* sc = a.vscale + (size_t)pass * LGP_TC_N;
 #pragma unroll
       for (int i = 0; i < LGP_TC_N; i += 2) {
-        const double x0 = acc[i] + comb[row * LGP_TC_N + i];
-        const double x1 = acc[i + 1] + comb[row * LGP_TC_N + i + 1];
+        const double x0 = (acc[i] + comb[row * LGP_TC_N + i]) * (double)sc[i];
+        const double x1 = (acc[i + 1] + comb[row * LGP_TC_N + i + 1]) * (double)sc[i + 1];
         reinterpret_cast<double2*>(out)[i / 2] = make_double2(x0, x1);
       }
     }
@@ -430,7 +499,6 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 #undef BAR
-#undef T_D1
-#undef T_L
+#undef T_SB
 #undef T_D2
 }

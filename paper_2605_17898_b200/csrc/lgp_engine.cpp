@@ -9,6 +9,8 @@
 // is identical on every rank, and no scalar all-reduce is needed.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "lgp_internal.h"
@@ -95,7 +97,9 @@ void MatvecOp::prepare() {
     // operands pre-tiled in the UMMA canonical layout, TF32 hi/lo split
     fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * 2 * plan.tc_kd * 4);
     fc = (float*)ctx->scratch_get(tag + ".b1", (size_t)n_cols_pad * 2 * plan.tc_kd * 4);
-    vtc = (float*)ctx->scratch_get(tag + ".vtc", (size_t)n_pass * n_cols_pad * 2 * tb * 4);
+    vtc = ctx->scratch_get(tag + ".vtc", (size_t)n_pass * n_cols_pad * 2 * tb * 2);
+    vscale = (float*)ctx->scratch_get(tag + ".vscale", (size_t)n_pass * tb * 4);
+    v_inexact = (int*)ctx->scratch_get(tag + ".vflag", 16);
     LgpPrepArgs pa = plan.prep;
     pa.x = rows->x;
     pa.ctr = cols->ctr;
@@ -170,8 +174,10 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     ctx->ev_pending.push_back(ev);
   };
   if (plan.tc) {
-    vec::pack_rhs_tc(ctx, V_dev, cols->n, t, n_tiles, tb, n_pass, vtc, done);
+    vec::pack_rhs_tc(ctx, V_dev, cols->n, t, n_tiles, tb, n_pass, vtc, vscale, v_inexact, done);
     LgpTcArgs a = plan.tca;
+    a.v_inexact = v_inexact;
+    a.vscale = vscale;
     a.a1 = fr;
     a.b1 = fc;
     a.v = vtc;
@@ -185,9 +191,27 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     a.n_tiles = n_tiles;
     const int64_t grid = (int64_t)n_rb * n_seg * n_pass;
     if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
+    unsigned long long* trace = nullptr;
+    if (std::getenv("LGP_TC_TRACE")) {
+      trace = (unsigned long long*)ctx->scratch_get("tc.trace", 16 * 8);
+      LGP_CUDA_CHECK(cudaMemsetAsync(trace, 0, 16 * 8, ctx->stream));
+    }
+    a.trace = trace;
     prof_begin();
     launch(ctx, mod->matvec, (unsigned)grid, 1, 320, plan.smem_bytes, &a);
     prof_end();
+    if (trace) {
+      unsigned long long h[16];
+      LGP_CUDA_CHECK(cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+      LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+      const double ctas = (double)grid;
+      fprintf(stderr,
+              "[tc trace, cycles per CTA] producer: issue %.0f wait_empty %.0f | mma: "
+              "pre %.0f wait_sfull %.0f gemm1+ %.0f wait_pfull %.0f wait_d2e %.0f gemm2 %.0f | "
+              "wg(per warp): wait_d1 %.0f epi %.0f drain %.0f\n",
+              h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas,
+              h[6] / ctas, h[7] / ctas, h[9] / ctas / 8, h[10] / ctas / 8, h[11] / ctas / 8);
+    }
     vec::epilogue(ctx, partial, n_seg, n_pass, n_rows_pad, tb, n_rows, t, plan.root_scale, noise,
                   noise_v, out_dev, done);
     return;

@@ -195,7 +195,9 @@ struct MatvecOp {
   float* fr = nullptr;
   float* fc = nullptr;
   double* vpack = nullptr;
-  float* vtc = nullptr;
+  void* vtc = nullptr;
+  float* vscale = nullptr;
+  int* v_inexact = nullptr;
   double* partial = nullptr;
   int n_rows_pad = 0, n_cols_pad = 0, n_rb = 0, n_seg = 0, n_pass = 0, n_tiles = 0,
       tiles_per_seg = 0;
@@ -223,7 +225,7 @@ void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int 
 // RHS tiles for the tensor-core K1: [n_pass][n_tiles][hi,lo][tbn x 64] TF32 split,
 // UMMA K-major canonical layout
 void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int tbn, int n_pass,
-                 float* out, const int* done);
+                 void* out, float* scale, int* inexact, const int* done);
 void epilogue(Context* c, const double* partial, int n_seg, int n_pass, int64_t rows_pad, int tb,
               int64_t n_rows, int t, double scale, double noise, const double* noise_v,
               double* out, const int* done);

@@ -13,6 +13,7 @@
 // rounding sequence (no FMA contraction): x += step*p, r -= step*ap,
 // p = p*beta + r (solvers.py:115-121); w = w - a*q, w -= b*q_prev,
 // w -= B^T (B w) (solvers.py:143-147).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "lgp_internal.h"
@@ -81,8 +82,39 @@ __global__ void k_pack(const double* __restrict__ V, long long n, int t, long lo
   }
 }
 
+// power-of-two scale of each RHS column (max |V[:, c]| in [0.5, 1) after scaling)
+__global__ void k_colscale(const double* __restrict__ V, long long n, int t, int ncols_pad,
+                           float* scale, const int* done) {
+  __shared__ double sm[256];
+  if (is_done(done)) return;
+  const int c = blockIdx.x;
+  double m = 0.0;
+  if (c < t)
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(V[i * t + c]));
+  sm[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double sc = 1.0;
+    if (sm[0] > 0.0) {
+      int e;
+      frexp(sm[0], &e);
+      sc = ldexp(1.0, e);
+    }
+    scale[c] = (float)sc;
+  }
+  (void)ncols_pad;
+}
+
+// RHS tiles for the tensor-core K1: FP16 hi/lo of V / scale in the UMMA
+// K-major canonical layout (rows = RHS c, K = column jj; 8-row groups of
+// 8 x 128 B, 16-byte K chunks 128 B apart)
 __global__ void k_pack_tc(const double* __restrict__ V, long long n, int t, int n_tiles, int tbn,
-                          int n_pass, float* __restrict__ out, const int* done) {
+                          int n_pass, const float* __restrict__ scale, __half* __restrict__ out,
+                          int* inexact, const int* done) {
   if (is_done(done)) return;
   const long long total = (long long)n_pass * n_tiles * tbn * 64;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -94,16 +126,14 @@ __global__ void k_pack_tc(const double* __restrict__ V, long long n, int t, int 
     const int pass = (int)(pt / n_tiles);
     const long long j = tile * 64 + jj;
     const int col = pass * tbn + c;
-    const double v = (j < n && col < t) ? V[j * t + col] : 0.0;
-    const float f = (float)v;
-    const float hi = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
-    const float lo = (float)(v - (double)hi);
-    // K-major canonical tile (rows = RHS c, K = column jj): 8-row groups of
-    // 16 x 128 B, K halves 128 B apart
-    const int off = (c >> 3) * 512 + (jj >> 2) * 32 + (c & 7) * 4 + (jj & 3);
-    float* base = out + pt * 2 * tbn * 64;
+    const double v = (j < n && col < t) ? V[j * t + col] / (double)scale[col] : 0.0;
+    const __half hi = __float2half_rn((float)v);
+    const __half lo = __float2half_rn((float)(v - (double)__half2float(hi)));
+    const int off = (c >> 3) * 512 + (jj >> 3) * 64 + (c & 7) * 8 + (jj & 7);
+    __half* base = out + pt * 2 * tbn * 64;
     base[off] = hi;
     base[tbn * 64 + off] = lo;
+    if (__half2float(lo) != 0.0f && *inexact == 0) atomicOr(inexact, 1);
   }
 }
 
@@ -421,9 +451,12 @@ void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int 
 }
 
 void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int tbn, int n_pass,
-                 float* out, const int* done) {
+                 void* out, float* scale, int* inexact, const int* done) {
+  k_colscale<<<n_pass * tbn, 256, 0, c->stream>>>(V, n, t, n_pass * tbn, scale, done);
+  LGP_LAUNCH_CHECK(c);
+  LGP_CUDA_CHECK(cudaMemsetAsync(inexact, 0, sizeof(int), c->stream));
   k_pack_tc<<<grid_for((long long)n_pass * n_tiles * tbn * 64), 256, 0, c->stream>>>(
-      V, n, t, n_tiles, tbn, n_pass, out, done);
+      V, n, t, n_tiles, tbn, n_pass, scale, (__half*)out, inexact, done);
   LGP_LAUNCH_CHECK(c);
 }
 
