@@ -364,11 +364,13 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       const bool v_exact = a.v_inexact != nullptr && *a.v_inexact == 0;
       lgp_mbar_wait(BAR(B_AFULL), 0);
       int g1 = 0, g2 = 0;
+      TR_DECL
       while (g2 < nch) {
         // distance GEMM of chunk g1 into S buffer g1 % 4 (free once the
         // contraction of chunk g1 - 4 is issued: the tensor pipe is in order)
         if (g1 < nch && g1 < g2 + 4 &&
             lgp_mbar_test(BAR(B_SFULL(g1 % LGP_TC_STAGES)), (g1 / LGP_TC_STAGES) & 1)) {
+          TR_MARK(2)
           lgp_tc_fence_after();
           const int s = g1 % LGP_TC_STAGES;
           const unsigned long long b_hi = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
@@ -382,15 +384,18 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
             lgp_mma_tf32_ss(d, a_lo + o, b_hi + o, idesc1, 1);
           }
           lgp_mma_commit(BAR(B_S1FULL(g1 & 3)));
+          TR_MARK(3)
           ++g1;
           continue;
         }
         if (g2 < g1 && lgp_mbar_test(BAR(B_PFULL(g2 & 3)), (g2 >> 2) & 1)) {
+          TR_MARK(4)
           const int cc = g2;
           const int w = cc & 1, k = cc >> 1, gi = k / LGP_TC_G, b = gi & 1;
           const bool first = (k % LGP_TC_G) == 0;
           const bool last = ((k % LGP_TC_G) == LGP_TC_G - 1) || (cc + 2 >= nch);
           if (first && gi >= 2) lgp_mbar_wait(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
+          TR_MARK(6)
           lgp_tc_fence_after();
           const int s = cc % LGP_TC_STAGES;
           const unsigned long long v_hi =
@@ -407,6 +412,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
           }
           lgp_mma_commit(BAR(B_SEMPTY(s)));
           if (last) lgp_mma_commit(BAR(B_D2FULL(w, b)));
+          TR_MARK(7)
           ++g2;
         }
       }
