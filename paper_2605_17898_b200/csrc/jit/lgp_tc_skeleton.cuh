@@ -29,21 +29,28 @@
 // FP16 hi | lo in place) + 2x2 D2 accumulators.
 
 #ifdef LGP_TC_TRACE
-#define TR_DECL unsigned long long tr_t = clock64();
-#define TR_MARK(slot) { const unsigned long long n_ = clock64(); atomicAdd(a.trace + (slot), n_ - tr_t); tr_t = n_; }
+#define TR_DECL unsigned long long tr_t = clock64(); unsigned long long tr_acc[12] = {0,0,0,0,0,0,0,0,0,0,0,0};
+#define TR_MARK(slot) { const unsigned long long n_ = clock64(); tr_acc[slot] += n_ - tr_t; tr_t = n_; }
+#define TR_FLUSH(lo, hi) { for (int q_ = lo; q_ <= hi; ++q_) atomicAdd(a.trace + q_, tr_acc[q_]); }
 #else
+#define TR_FLUSH(lo, hi)
 #define TR_DECL
 #define TR_MARK(slot)
 #endif
 
+#ifndef LGP_TC_PRIO
+#define LGP_TC_PRIO 1
+#endif
 #ifndef LGP_TC_ABLATE
 #define LGP_TC_ABLATE 0
 #endif
 
 #ifdef LGP_TC_TRACE
-#define TR_DECL unsigned long long tr_t = clock64();
-#define TR_MARK(slot) { const unsigned long long n_ = clock64(); atomicAdd(a.trace + (slot), n_ - tr_t); tr_t = n_; }
+#define TR_DECL unsigned long long tr_t = clock64(); unsigned long long tr_acc[12] = {0,0,0,0,0,0,0,0,0,0,0,0};
+#define TR_MARK(slot) { const unsigned long long n_ = clock64(); tr_acc[slot] += n_ - tr_t; tr_t = n_; }
+#define TR_FLUSH(lo, hi) { for (int q_ = lo; q_ <= hi; ++q_) atomicAdd(a.trace + q_, tr_acc[q_]); }
 #else
+#define TR_FLUSH(lo, hi)
 #define TR_DECL
 #define TR_MARK(slot)
 #endif
@@ -346,6 +353,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
                      vbase + ((size_t)pass * a.n_tiles + tile0 + c) * TC_V_BYTES, TC_V_BYTES,
                      BAR(B_SFULL(s)));
       }
+      TR_FLUSH(0, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -368,6 +376,9 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       while (g2 < nch) {
         // distance GEMM of chunk g1 into S buffer g1 % 4 (free once the
         // contraction of chunk g1 - 4 is issued: the tensor pipe is in order)
+#if LGP_TC_PRIO == 2
+        if (g2 < g1 && lgp_mbar_test(BAR(B_PFULL(g2 & 3)), (g2 >> 2) & 1)) goto do_gemm2;
+#endif
         if (g1 < nch && g1 < g2 + 4 &&
             lgp_mbar_test(BAR(B_SFULL(g1 % LGP_TC_STAGES)), (g1 / LGP_TC_STAGES) & 1)) {
           TR_MARK(2)
@@ -389,6 +400,9 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
           continue;
         }
         if (g2 < g1 && lgp_mbar_test(BAR(B_PFULL(g2 & 3)), (g2 >> 2) & 1)) {
+#if LGP_TC_PRIO == 2
+        do_gemm2:
+#endif
           TR_MARK(4)
           const int cc = g2;
           const int w = cc & 1, k = cc >> 1, gi = k / LGP_TC_G, b = gi & 1;
@@ -416,6 +430,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
           ++g2;
         }
       }
+      TR_FLUSH(2, 7)
     }
     __syncwarp();
   } else {
@@ -478,6 +493,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       if (lane == 0) { TR_MARK(11) }
     }
     if (nloc >= 1) drain((nloc - 1) / LGP_TC_G);
+    if (lane == 0) { TR_FLUSH(8, 11) }
 
     // combine the two warpgroups' FP64 sums in a fixed order, undo the V scaling
     if (w == 1) {

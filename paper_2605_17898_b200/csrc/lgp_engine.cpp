@@ -207,7 +207,7 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
       const double ctas = (double)grid;
       fprintf(stderr,
               "[tc trace, cycles per CTA] producer: issue %.0f wait_empty %.0f | mma: "
-              "idle->g1 %.0f gemm1 %.0f idle->g2 %.0f - %.0f wait_d2e %.0f gemm2 %.0f | "
+              "poll %.0f gemm1 %.0f poll %.0f - %.0f wait_d2e %.0f gemm2 %.0f | "
               "wg(per warp): wait_d1 %.0f epi %.0f drain %.0f\n",
               h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas,
               h[6] / ctas, h[7] / ctas, h[9] / ctas / 8, h[10] / ctas / 8, h[11] / ctas / 8);

@@ -91,3 +91,24 @@ def test_no_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(G.MiniGpError, match="no CUDA device"):
         _lib.Context(0)
+
+
+def test_tensor_core_jit_compiles_with_tcgen05():
+    import glob
+    import subprocess
+
+    log = G.kernels.program(G.parse_kernel("(rbf 0.5)")).jit(8, 16)
+    assert "[tensor-core module]" in log and "'lgp_matvec_tc'" in log
+    tc = log.split("[tensor-core module]")[1]
+    m = re.search(r"'lgp_matvec_tc'.*?(\d+) bytes spill stores", tc, re.S)
+    assert m and m.group(1) == "0"
+    # the cached cubin's SASS proves tcgen05 MMA, TMEM ld/st and TMA bulk copies
+    src = G.kernels.program(G.parse_kernel("(rbf 0.5)")).source(8, 16)
+    cache = os.path.join(ROOT, "paper_2605_17898_b200", "_lib", "jit_cache")
+    cubins = [p for p in glob.glob(os.path.join(cache, "*.cu"))
+              if open(p).read().strip() == src.strip()]
+    assert cubins, "tensor-core module not in the JIT cache"
+    sass = subprocess.run(["cuobjdump", "-sass", cubins[0][:-3] + ".cubin"], capture_output=True,
+                          text=True).stdout
+    for mnemonic in ("UTCHMMA", "LDTM", "STTM", "UBLKCP", "MUFU.EX2"):
+        assert mnemonic in sass, mnemonic

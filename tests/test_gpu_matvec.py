@@ -217,3 +217,51 @@ def test_reference_kernel_objects_are_accepted(gpu_ctx):
     got = G.KernelOperator(RBF(0.4), x, 0.1)(v)
     want = G.matrix_free_matvec(G.RBF(0.4), x, 0.1, v)
     np.testing.assert_array_equal(got, want)
+
+
+# ---- tensor-core K1 (tcgen05, 3xTF32 distance GEMM + FP16 hi/lo contraction)
+TC_CASES = [("(rbf 0.5)", 300, 8, 16), ("(rbf 0.5)", 1000, 8, 16), ("(matern52 0.7)", 777, 4, 8),
+            ("(+ (scale 2.0 (rbf 0.4)) (scale 0.5 (matern32 0.9)))", 2049, 6, 20),
+            ("(scale 1.5 (matern32 0.5))", 4096, 8, 16), ("(* (rbf 0.8) (matern52 1.1))", 129, 5, 33)]
+
+
+def _mv_flags(expr, x, V, noise, flags):
+    ctx = _lib.default_context()
+    prog = G.kernels.program(G.parse_kernel(expr))
+    pts = _lib.DevicePoints(ctx, x)
+    V = np.ascontiguousarray(V)
+    out = np.empty_like(V)
+    _lib.check(_lib.lib().lgp_matvec(ctx.handle, prog.handle, pts.handle, pts.handle, noise,
+                                     _lib.vptr(V), V.shape[1], _lib.vptr(out), flags))
+    return out
+
+
+@pytest.mark.parametrize("expr,n,d,t", TC_CASES)
+@pytest.mark.parametrize("kind", ["gauss", "probes"])
+def test_tensor_core_matvec_parity(gpu_ctx, expr, n, d, t, kind):
+    src = G.kernels.program(G.parse_kernel(expr)).source(d, t)
+    assert "lgp_matvec_tc" in src  # eligible tree / shape takes the tcgen05 kernel
+    rng = np.random.default_rng(n + t)
+    x = rng.random((n, d))
+    V = rng.standard_normal((n, t)) * 3.0 if kind == "gauss" else O.probes(n, t, seed=1)
+    tc = _mv_flags(expr, x, V, 0.1, 0)
+    simt = _mv_flags(expr, x, V, 0.1, _lib.FORCE_SIMT)
+    ref = O.matvec(O.parse_tree(expr), x, 0.1, V)
+    assert rel_l2(tc, ref) <= TOL
+    assert rel_l2(tc, simt) <= TOL  # the north star's bar: TC variant vs the FP32-SIMT kernel
+
+
+def test_tensor_core_not_used_where_ineligible():
+    for expr, d, t in [("(rbf 0.5)", 8, 1), ("(rbf 0.2)", 1, 16), ("(matern12 0.5)", 8, 16),
+                       ("(+ (rbf 0.5) (periodic 1.0 1.0))", 4, 16), ("(linear 0.5)", 8, 16)]:
+        assert "lgp_matvec_tc" not in G.kernels.program(G.parse_kernel(expr)).source(d, t)
+
+
+def test_tensor_core_cfg4_rows(gpu_ctx):
+    g = golden("matvec_rows.npz")
+    cfg = O.CONFIGS["cfg4"]
+    x, _ = O.synthetic(cfg["n"], cfg["d"])
+    z = O.probes(cfg["n"], 16)
+    out = _mv_flags(cfg["kernel"], x, z, cfg["noise"], 0)
+    r0, r1 = (int(a) for a in g["cfg4_rows"])
+    assert rel_l2(out[r0:r1], g["cfg4_yz"]) <= TOL
