@@ -149,6 +149,8 @@ int lgp_ctx_destroy(lgp_ctx* ctx) {
   for (auto& kv : ctx->modules)
     if (kv.second->mod) drv::ModuleUnload(kv.second->mod);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+  for (auto& kv : ctx->pool)
+    for (void* q : kv.second) cudaFree(q);
   for (auto& ev : ctx->ev_pending) ctx->ev_pool.push_back(ev);
   for (auto& ev : ctx->ev_pool) {
     cudaEventDestroy(ev.first);
@@ -373,13 +375,15 @@ int lgp_points_upload(lgp_ctx* ctx, const double* X, int64_t n, int32_t d, lgp_p
     for (int j = 0; j < d; ++j) p->center[j] += X[i * d + j];
   if (n > 0)
     for (int j = 0; j < d; ++j) p->center[j] /= (double)n;
-  LGP_CUDA_CHECK(cudaMalloc(&p->x, (size_t)std::max<int64_t>(n, 1) * d * 8));
-  LGP_CUDA_CHECK(cudaMalloc(&p->ctr, (size_t)d * 8));
+  const size_t xbytes = ((size_t)std::max<int64_t>(n, 1) * d * 8 + 255) / 256 * 256;
+  p->bytes = xbytes + (size_t)d * 8;
+  p->x = (double*)ctx->pool_get(p->bytes);
+  p->ctr = (double*)((char*)p->x + xbytes);
   if (n > 0)
     LGP_CUDA_CHECK(cudaMemcpyAsync(p->x, X, (size_t)n * d * 8, cudaMemcpyHostToDevice, ctx->stream));
   LGP_CUDA_CHECK(cudaMemcpyAsync(p->ctr, p->center.data(), (size_t)d * 8, cudaMemcpyHostToDevice,
                                  ctx->stream));
-  LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // the host X may be freed after return
   *out = p.release();
   API_END
 }
@@ -388,10 +392,8 @@ int lgp_points_free(lgp_points* p) {
   API_BEGIN
   if (!p) return LGP_OK;
   std::lock_guard<std::recursive_mutex> g(p->ctx->mu);
-  p->ctx->activate();
-  cudaStreamSynchronize(p->ctx->stream);
-  cudaFree(p->x);
-  cudaFree(p->ctr);
+  // stream-ordered reuse: later work on the context stream may recycle it
+  p->ctx->pool_put(p->x, p->bytes);
   delete p;
   API_END
 }

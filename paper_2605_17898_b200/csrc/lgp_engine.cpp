@@ -19,6 +19,29 @@ namespace lgp {
 
 void Context::activate() { LGP_CUDA_CHECK(cudaSetDevice(device)); }
 
+size_t Context::pool_round(size_t bytes) {
+  size_t r = 4096;
+  while (r < bytes) r <<= 1;
+  return r;
+}
+
+void* Context::pool_get(size_t bytes) {
+  const size_t r = pool_round(bytes);
+  auto& v = pool[r];
+  if (!v.empty()) {
+    void* p = v.back();
+    v.pop_back();
+    return p;
+  }
+  void* p = nullptr;
+  LGP_CUDA_CHECK(cudaMalloc(&p, r));
+  return p;
+}
+
+void Context::pool_put(void* p, size_t bytes) {
+  if (p) pool[pool_round(bytes)].push_back(p);
+}
+
 void* Context::scratch_get(const std::string& name, size_t bytes) {
   if (bytes == 0) bytes = 16;
   DeviceBuffer& b = scratch[name];

@@ -149,6 +149,12 @@ struct Context {
   double prof_ms = 0.0;
   uint64_t prof_count = 0;
 
+  // stream-ordered pool for point sets (no cudaMalloc / cudaFree + sync per call)
+  std::map<size_t, std::vector<void*>> pool;
+  void* pool_get(size_t bytes);
+  void pool_put(void* p, size_t bytes);
+  static size_t pool_round(size_t bytes);
+
   void* scratch_get(const std::string& name, size_t bytes);  // grow-only
   void activate();  // cudaSetDevice for the calling thread
 };
@@ -162,8 +168,9 @@ struct Points {
   Context* ctx;
   int64_t n = 0;
   int32_t d = 0;
-  double* x = nullptr;        // device n x d FP64
+  double* x = nullptr;        // device n x d FP64, followed by ctr (one pooled block)
   double* ctr = nullptr;      // device d FP64: column mean (centring of features)
+  size_t bytes = 0;           // pooled block size
   std::vector<double> center; // host copy of ctr
 };
 

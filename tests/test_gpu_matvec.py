@@ -60,9 +60,10 @@ def test_matvec_full_size_rows_vs_reference(gpu_ctx, name):
         z = O.probes(cfg["n"], cfg["t"])
         outz = op(z)
         assert rel_l2(outz[r0:r1], g[f"{name}_yz"]) <= TOL
-        # column c of the block equals the single-RHS product (to accumulation order)
+        # column c of the block equals the single-RHS product (the block may take the
+        # tensor-core kernel, the single column the FP64-accumulating SIMT one)
         one = op(np.ascontiguousarray(z[:, 1]))
-        assert rel_l2(outz[:, 1], one) <= 1e-12
+        assert rel_l2(outz[:, 1], one) <= TOL
 
 
 def test_reference_unit_cases(gpu_ctx):
