@@ -75,6 +75,7 @@ extern "C" {
 #define LGP_ACC_FP32 2u      /* matvec: FP32 accumulation variant (default FP64) */
 #define LGP_DIST_DIRECT 4u   /* matvec: direct differences instead of the norm trick */
 #define LGP_FORCE_SIMT 8u    /* matvec: never use the tensor-core (tcgen05) kernel */
+#define LGP_NO_SYM 16u       /* matvec: no symmetric block-pair kernel for the square operator */
 
 typedef struct lgp_ctx lgp_ctx;
 typedef struct lgp_kernel lgp_kernel;

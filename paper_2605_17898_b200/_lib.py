@@ -35,6 +35,7 @@ DEVICE_PTRS = 1
 ACC_FP32 = 2
 DIST_DIRECT = 4
 FORCE_SIMT = 8
+NO_SYM = 16
 
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)

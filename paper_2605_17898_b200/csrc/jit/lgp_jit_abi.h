@@ -33,7 +33,9 @@ struct LgpMatvecArgs {
   int n_pass;           // RHS passes of TB columns
   int tiles_per_seg;
   int n_tiles;          // column tiles in total
-  int pad_;
+  int n_units;          // symmetric kernel: block pairs (I, J >= I)
+  const int* units;     // symmetric kernel: [n_units][2] = (I, J)
+  double* colpart;      // symmetric kernel: column-side partials, like partial
   float kc[LGP_MAX_KC];
 };
 

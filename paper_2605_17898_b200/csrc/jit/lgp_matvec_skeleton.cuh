@@ -249,6 +249,158 @@ extern "C" __global__ void __launch_bounds__(LGP_THREADS, LGP_MINB)
   }
 }
 
+
+// --------------------------------------------------- K1, symmetric operator
+// K(X, X) is symmetric, so every off-diagonal block pair (I, J > I) is
+// evaluated once and used twice: row side  out_I += K_IJ V_J  (registers) and
+// column side out_J += K_IJ^T V_I (per-column warp reduction, then a fixed-
+// order combine over warps). Diagonal blocks are evaluated in full, row side
+// only. Halves the distance + transcendental work of the square operator;
+// the FP32 entry k_ij is the same number on both sides, so the operator stays
+// exactly symmetric. Partials are written per block pair and reduced in a
+// fixed order by the epilogue (deterministic).
+extern "C" __global__ void __launch_bounds__(LGP_THREADS, LGP_MINB)
+    lgp_matvec_sym(const LgpMatvecArgs a) {
+  if (a.done != nullptr && *a.done) return;
+  const int unit = blockIdx.x;
+  const int pass = blockIdx.y;
+  const int I = a.units[2 * unit], J = a.units[2 * unit + 1];
+  const bool offdiag = J != I;
+  constexpr int TPB = LGP_ROWS_PER_CTA / LGP_CC;  // column tiles per block
+  const int tile0 = J * TPB;
+  const int ntiles = TPB;
+
+  extern __shared__ __align__(128) unsigned char lgp_smem[];
+  float* feat_s = reinterpret_cast<float*>(lgp_smem);
+  double* v_s = reinterpret_cast<double*>(lgp_smem + LGP_STAGES * LGP_FEAT_TILE_BYTES);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(
+      lgp_smem + LGP_STAGES * (LGP_FEAT_TILE_BYTES + LGP_V_TILE_BYTES));
+  double* colbuf = reinterpret_cast<double*>(bars + 2 * LGP_STAGES);  // [NWARPS][CC][TB]
+  const unsigned full0 = lgp_saddr(bars);
+  const unsigned empty0 = lgp_saddr(bars + LGP_STAGES);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int wid = tid >> 5;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < LGP_STAGES; ++s) {
+      lgp_mbar_init(full0 + 8 * s, 1);
+      lgp_mbar_init(empty0 + 8 * s, LGP_NWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const double* v_g = a.v + (size_t)pass * a.n_cols_pad * LGP_TB;
+  auto issue = [&](int stage, int tile) {
+    const unsigned bar = full0 + 8 * stage;
+    lgp_mbar_expect_tx(bar, LGP_FEAT_TILE_BYTES + LGP_V_TILE_BYTES);
+    lgp_bulk_g2s(lgp_saddr(feat_s + stage * (LGP_CC * LGP_FC)),
+                 a.fc + (size_t)tile * LGP_CC * LGP_FC, LGP_FEAT_TILE_BYTES, bar);
+    lgp_bulk_g2s(lgp_saddr(v_s + stage * (LGP_CC * LGP_TB)),
+                 v_g + (size_t)tile * LGP_CC * LGP_TB, LGP_V_TILE_BYTES, bar);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < LGP_STAGES && s < ntiles; ++s) issue(s, tile0 + s);
+  }
+
+  float fr[LGP_R][LGP_FR];
+  double vr[LGP_R][LGP_TB];
+  const int row_base = I * LGP_ROWS_PER_CTA + tid;
+#pragma unroll
+  for (int r = 0; r < LGP_R; ++r) {
+    const int row = row_base + r * LGP_THREADS;
+    const float4* src = reinterpret_cast<const float4*>(a.fr + (size_t)row * LGP_FR);
+#pragma unroll
+    for (int q = 0; q < LGP_FR / 4; ++q) {
+      const float4 f4 = src[q];
+      fr[r][4 * q] = f4.x;
+      fr[r][4 * q + 1] = f4.y;
+      fr[r][4 * q + 2] = f4.z;
+      fr[r][4 * q + 3] = f4.w;
+    }
+#pragma unroll
+    for (int c = 0; c < LGP_TB; ++c) vr[r][c] = v_g[(size_t)row * LGP_TB + c];
+  }
+
+  double acc[LGP_R][LGP_TB];
+#pragma unroll
+  for (int r = 0; r < LGP_R; ++r)
+#pragma unroll
+    for (int c = 0; c < LGP_TB; ++c) acc[r][c] = 0.0;
+
+  double* colp = a.colpart + ((size_t)unit * gridDim.y + pass) * LGP_ROWS_PER_CTA * LGP_TB;
+  for (int it = 0; it < ntiles; ++it) {
+    const int st = it % LGP_STAGES;
+    const unsigned ph = (unsigned)(it / LGP_STAGES) & 1u;
+    lgp_mbar_wait(full0 + 8 * st, ph);
+    const float4* F = reinterpret_cast<const float4*>(feat_s + st * (LGP_CC * LGP_FC));
+    const double* V = v_s + st * (LGP_CC * LGP_TB);
+#pragma unroll 2
+    for (int j = 0; j < LGP_CC; ++j) {
+      float fc[LGP_FC];
+#pragma unroll
+      for (int q = 0; q < LGP_FC / 4; ++q) {
+        const float4 f4 = F[j * (LGP_FC / 4) + q];
+        fc[4 * q] = f4.x;
+        fc[4 * q + 1] = f4.y;
+        fc[4 * q + 2] = f4.z;
+        fc[4 * q + 3] = f4.w;
+      }
+      double vj[LGP_TB];
+#pragma unroll
+      for (int c = 0; c < LGP_TB; ++c) vj[c] = V[j * LGP_TB + c];
+      double col[LGP_TB];
+#pragma unroll
+      for (int c = 0; c < LGP_TB; ++c) col[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < LGP_R; ++r) {
+        const double kd = lgp_widen(lgp_entry(fr[r], fc, a));
+#pragma unroll
+        for (int c = 0; c < LGP_TB; ++c) {
+          acc[r][c] = fma(kd, vj[c], acc[r][c]);
+          col[c] = fma(kd, vr[r][c], col[c]);
+        }
+      }
+      if (offdiag) {
+#pragma unroll
+        for (int c = 0; c < LGP_TB; ++c) {
+          double v = col[c];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == (j & 31)) colbuf[(wid * LGP_CC + j) * LGP_TB + c] = v;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) lgp_mbar_arrive(empty0 + 8 * st);
+    if (tid == 0 && it + LGP_STAGES < ntiles) {
+      lgp_mbar_wait(empty0 + 8 * st, ph);
+      issue(st, tile0 + it + LGP_STAGES);
+    }
+    if (offdiag) {
+      __syncthreads();
+      for (int e = tid; e < LGP_CC * LGP_TB; e += LGP_THREADS) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < LGP_NWARPS; ++w) s += colbuf[w * LGP_CC * LGP_TB + e];
+        colp[(size_t)it * LGP_CC * LGP_TB + e] = s;
+      }
+      __syncthreads();
+    }
+  }
+
+  double* out = a.partial + ((size_t)unit * gridDim.y + pass) * LGP_ROWS_PER_CTA * LGP_TB;
+#pragma unroll
+  for (int r = 0; r < LGP_R; ++r) {
+    double* o = out + (size_t)(tid + r * LGP_THREADS) * LGP_TB;
+#pragma unroll
+    for (int c = 0; c < LGP_TB; ++c) o[c] = acc[r][c];
+  }
+}
+
 // ------------------------------------------------------- FP64 companions
 // Dense cross-covariance (kernel_eval) and diagonal (kernel_diag) in FP64,
 // evaluated with direct differences: exactly symmetric for rows == cols.

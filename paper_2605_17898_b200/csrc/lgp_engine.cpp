@@ -151,6 +151,29 @@ void MatvecOp::prepare() {
     ++ctx->launches;
     return;
   }
+  // symmetric block-pair kernel for the square operator on a single rank
+  sym = (rows == cols) && ctx->world == 1 && tb <= 4 && !(flags & LGP_NO_SYM) &&
+        (rows_per_cta % tu.cc) == 0 && n_rb >= 2;
+  if (sym) {
+    n_cols_pad = n_rows_pad;  // column blocks = row blocks
+    n_tiles = n_cols_pad / tu.cc;
+    n_units = n_rb * (n_rb + 1) / 2;
+    std::vector<int> tab((size_t)n_units * 2);
+    int u = 0;
+    for (int I = 0; I < n_rb; ++I)
+      for (int J = I; J < n_rb; ++J) {
+        tab[2 * u] = I;
+        tab[2 * u + 1] = J;
+        ++u;
+      }
+    units = (int*)ctx->scratch_get(tag + ".units", tab.size() * 4);
+    LGP_CUDA_CHECK(cudaMemcpyAsync(units, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+    const size_t pb = (size_t)n_units * n_pass * rows_per_cta * tb * 8;
+    partial = (double*)ctx->scratch_get(tag + ".part", pb);
+    colpart = (double*)ctx->scratch_get(tag + ".colp", pb);
+    smem_sym = plan.smem_bytes + (size_t)(tu.threads / 32) * tu.cc * tb * 8;
+  }
   fr = (float*)ctx->scratch_get(tag + ".fr", (size_t)n_rows_pad * plan.fr * 4);
   fc = (float*)ctx->scratch_get(tag + ".fc", (size_t)n_cols_pad * plan.fc * 4);
   vpack = (double*)ctx->scratch_get(tag + ".v", (size_t)n_pass * n_cols_pad * tb * 8);
@@ -240,6 +263,32 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     return;
   }
   vec::pack_rhs(ctx, V_dev, cols->n, t, n_cols_pad, tb, n_pass, vpack, done);
+  if (sym) {
+    LgpMatvecArgs a = plan.mv;
+    a.fr = fr;
+    a.fc = fc;
+    a.v = vpack;
+    a.partial = partial;
+    a.colpart = colpart;
+    a.units = units;
+    a.n_units = n_units;
+    a.done = done;
+    a.n_rows_pad = n_rows_pad;
+    a.n_cols_pad = n_cols_pad;
+    a.n_rb = n_rb;
+    a.n_tiles = n_tiles;
+    a.n_pass = n_pass;
+    prof_begin();
+    void* params[] = {&a};
+    LGP_CU_CHECK(drv::LaunchKernel(mod->matvec_sym, (unsigned)n_units, (unsigned)n_pass, 1,
+                                   plan.tune.threads, 1, 1, (unsigned)smem_sym,
+                                   (CUstream)ctx->stream, params, nullptr));
+    ++ctx->launches;
+    prof_end();
+    vec::sym_epilogue(ctx, partial, colpart, n_rb, plan.tune.threads * plan.tune.r, n_pass, tb,
+                      n_rows, t, plan.root_scale, noise, noise_v, out_dev, done);
+    return;
+  }
   LgpMatvecArgs a = plan.mv;
   a.fr = fr;
   a.fc = fc;

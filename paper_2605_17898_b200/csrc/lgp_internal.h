@@ -111,6 +111,7 @@ Plan make_tc_plan(const Tree& tree, int d, int t, uint32_t flags);
 struct Module {
   CUmodule mod = nullptr;
   CUfunction prep = nullptr, matvec = nullptr, gram = nullptr, diag = nullptr;
+  CUfunction matvec_sym = nullptr;  // symmetric-operator K1 (SIMT modules)
   bool tc = false;  // module holds lgp_tc_prep / lgp_matvec_tc in prep / matvec
   int blocks_per_sm = 1;
   int regs = 0;
@@ -199,6 +200,11 @@ struct MatvecOp {
   Plan plan;
   Module* mod = nullptr;
   bool allow_tc = false;  // may use the tensor-core K1 (matvec API, Lanczos; not CG)
+  bool sym = false;       // square operator on one rank: symmetric block-pair kernel
+  int n_units = 0;
+  int* units = nullptr;
+  double* colpart = nullptr;
+  size_t smem_sym = 0;
   float* fr = nullptr;
   float* fc = nullptr;
   double* vpack = nullptr;
@@ -236,6 +242,10 @@ void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int
 void epilogue(Context* c, const double* partial, int n_seg, int n_pass, int64_t rows_pad, int tb,
               int64_t n_rows, int t, double scale, double noise, const double* noise_v,
               double* out, const int* done);
+// symmetric kernel: out_i = sum_{J>=B} rowp[(B,J)] + sum_{I<B} colp[(I,B)], fixed order
+void sym_epilogue(Context* c, const double* rowp, const double* colp, int nb, int rb, int n_pass,
+                  int tb, int64_t n, int t, double scale, double noise, const double* noise_v,
+                  double* out, const int* done);
 // column dots: part[blk][t] then final[t] (deterministic order)
 void dot_partial(Context* c, const double* a, const double* b, int64_t n, int t, double* part,
                  const int* done);

@@ -176,6 +176,12 @@ Module* get_module(Context* ctx, const Plan& plan) {
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->matvec, m->mod, "lgp_matvec"));
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->gram, m->mod, "lgp_gram"));
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->diag, m->mod, "lgp_diag"));
+    LGP_CU_CHECK(drv::ModuleGetFunction(&m->matvec_sym, m->mod, "lgp_matvec_sym"));
+    const size_t sym_smem = plan.smem_bytes + (size_t)(plan.tune.threads / 32) * plan.tune.cc *
+                                                  plan.tune.tb * 8;
+    LGP_CU_CHECK(drv::FuncSetAttribute(m->matvec_sym,
+                                       CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                       (int)sym_smem));
   }
   LGP_CU_CHECK(drv::FuncSetAttribute(m->matvec, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                                   (int)plan.smem_bytes));

@@ -156,6 +156,33 @@ __global__ void k_epilogue(const double* __restrict__ partial, int n_seg, int n_
   }
 }
 
+__global__ void k_sym_epilogue(const double* __restrict__ rowp, const double* __restrict__ colp,
+                               int nb, int rb, int n_pass, int tb, long long n, int t,
+                               double scale, double noise, const double* __restrict__ noise_v,
+                               double* __restrict__ out, const int* done) {
+  if (is_done(done)) return;
+  const long long total = n * t;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / t;
+    const int c = (int)(e % t);
+    const int p = c / tb, cc = c % tb;
+    const int B = (int)(i / rb), il = (int)(i % rb);
+    double s = 0.0;
+    // row side of the block pairs (B, J >= B), then column side of (I < B, B)
+    const long long uB = (long long)B * nb - (long long)B * (B - 1) / 2;
+    for (int J = B; J < nb; ++J)
+      s += rowp[(((uB + (J - B)) * n_pass + p) * rb + il) * tb + cc];
+    for (int I = 0; I < B; ++I) {
+      const long long u = (long long)I * nb - (long long)I * (I - 1) / 2 + (B - I);
+      s += colp[((u * n_pass + p) * rb + il) * tb + cc];
+    }
+    double o = __dmul_rn(scale, s);
+    if (noise_v != nullptr && noise != 0.0) o = __dadd_rn(o, __dmul_rn(noise, noise_v[e]));
+    out[e] = o;
+  }
+}
+
 __global__ void k_fill(double* p, long long n, double v) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x)
@@ -465,6 +492,14 @@ void epilogue(Context* c, const double* partial, int n_seg, int n_pass, int64_t 
               double* out, const int* done) {
   k_epilogue<<<grid_for(n_rows * t), 256, 0, c->stream>>>(
       partial, n_seg, n_pass, rows_pad, tb, n_rows, t, scale, noise, noise_v, out, done);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void sym_epilogue(Context* c, const double* rowp, const double* colp, int nb, int rb, int n_pass,
+                  int tb, int64_t n, int t, double scale, double noise, const double* noise_v,
+                  double* out, const int* done) {
+  k_sym_epilogue<<<grid_for(n * t), 256, 0, c->stream>>>(rowp, colp, nb, rb, n_pass, tb, n, t,
+                                                         scale, noise, noise_v, out, done);
   LGP_LAUNCH_CHECK(c);
 }
 
