@@ -152,7 +152,7 @@ void MatvecOp::prepare() {
     return;
   }
   // symmetric block-pair kernel for the square operator on a single rank
-  sym = (rows == cols) && ctx->world == 1 && tb <= 4 && !(flags & LGP_NO_SYM) &&
+  sym = (rows == cols) && ctx->world == 1 && tb == 1 && !(flags & LGP_NO_SYM) &&
         (rows_per_cta % tu.cc) == 0 && n_rb >= 2;
   if (sym) {
     n_cols_pad = n_rows_pad;  // column blocks = row blocks
