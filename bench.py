@@ -344,9 +344,12 @@ def run_ours(args, rank, world):
             traffic = json.load(f).get(args.config)
     except Exception:
         pass
+    tc = "lgp_matvec_tc" in prog.source(d, t)
     roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": traffic,
-                "kernel": "lgp_matvec (fused K1)", "k1_ms_per_launch": k1_avg_ms,
+                "kernel": ("lgp_matvec_tc (fused K1, tcgen05 3xTF32 distance GEMM + FP16x2 "
+                           "contraction)" if tc else "lgp_matvec (fused K1, SIMT FP32/FP64)"),
+                "k1_ms_per_launch": k1_avg_ms,
                 "flops_per_entry": flops, "sfu_per_entry": sfu,
                 "peak_source": f"derived: 2 x {FP32_LANES} FP32 lanes x {SM_COUNT} SMs x "
                                f"{f_mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)",

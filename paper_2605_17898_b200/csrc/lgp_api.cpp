@@ -4,6 +4,8 @@
 // returns a status code; the message is kept per thread.
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
 
 #include "lgp_internal.h"
@@ -16,6 +18,17 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 }  // namespace lgp
 
 struct lgp_ctx : Context {};
+
+namespace {
+// Live contexts: objects that outlive their context (point sets freed by a
+// garbage collector after the context) must not touch it.
+std::mutex g_ctx_mu;
+std::set<const Context*> g_live;
+bool ctx_alive(const Context* c) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  return g_live.count(c) != 0;
+}
+}  // namespace
 struct lgp_kernel : KernelHandle {};
 struct lgp_points : Points {};
 
@@ -135,6 +148,10 @@ int lgp_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, lgp_
   LGP_CUDA_CHECK(cudaEventCreate(&c->ev0));
   LGP_CUDA_CHECK(cudaEventCreate(&c->ev1));
   if (world > 1) c->comm = comm_create(rank, world, nccl_id, c->stream);
+  {
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    g_live.insert(c.get());
+  }
   *out = c.release();
   API_END
 }
@@ -142,6 +159,10 @@ int lgp_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, lgp_
 int lgp_ctx_destroy(lgp_ctx* ctx) {
   API_BEGIN
   if (!ctx) return LGP_OK;
+  {
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    if (!g_live.erase(ctx)) return LGP_OK;  // idempotent
+  }
   ctx->activate();
   cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->scratch)
@@ -391,9 +412,11 @@ int lgp_points_upload(lgp_ctx* ctx, const double* X, int64_t n, int32_t d, lgp_p
 int lgp_points_free(lgp_points* p) {
   API_BEGIN
   if (!p) return LGP_OK;
-  std::lock_guard<std::recursive_mutex> g(p->ctx->mu);
-  // stream-ordered reuse: later work on the context stream may recycle it
-  p->ctx->pool_put(p->x, p->bytes);
+  if (ctx_alive(p->ctx)) {
+    std::lock_guard<std::recursive_mutex> g(p->ctx->mu);
+    // stream-ordered reuse: later work on the context stream may recycle it
+    p->ctx->pool_put(p->x, p->bytes);
+  }
   delete p;
   API_END
 }
