@@ -56,7 +56,7 @@
 #endif
 
 #define TC_CH 64
-#define TC_THREADS 320
+#define TC_THREADS 352  // 11 warps: producer, 2 MMA issuers, 2 epilogue warpgroups
 #define TC_A1_FLOATS (128 * LGP_TC_KD)
 #define TC_B1_FLOATS (TC_CH * LGP_TC_KD)
 #define TC_V_HALFS (LGP_TC_N * TC_CH)
@@ -65,16 +65,20 @@
 #define TC_V_BYTES (2 * TC_V_HALFS * 2)
 #define TC_STAGE_BYTES (TC_B1_BYTES + TC_V_BYTES)
 #define TC_COMB_BYTES (128 * LGP_TC_N * 8)
-#define TC_NBARS (17 + 2 * LGP_TC_STAGES)
+#ifndef LGP_TC_NSB
+#define LGP_TC_NSB 6   // S buffers in TMEM (64 columns each), even: NSB/2 per warpgroup
+#endif
+#define TC_NSBW (LGP_TC_NSB / 2)
+#define TC_NBARS (9 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB)
 
 // barrier slots
 #define B_AFULL 0
 #define B_SFULL(s) (1 + (s))
 #define B_SEMPTY(s) (1 + LGP_TC_STAGES + (s))
 #define B_S1FULL(q) (1 + 2 * LGP_TC_STAGES + (q))
-#define B_PFULL(q) (5 + 2 * LGP_TC_STAGES + (q))
-#define B_D2FULL(w, b) (9 + 2 * LGP_TC_STAGES + 2 * (w) + (b))
-#define B_D2EMPTY(w, b) (13 + 2 * LGP_TC_STAGES + 2 * (w) + (b))
+#define B_PFULL(q) (1 + 2 * LGP_TC_STAGES + LGP_TC_NSB + (q))
+#define B_D2FULL(w, b) (1 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB + 2 * (w) + (b))
+#define B_D2EMPTY(w, b) (5 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB + 2 * (w) + (b))
 
 __device__ __forceinline__ float lgp_ex2(float x) {
   float y;
@@ -307,7 +311,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       lgp_mbar_init(BAR(B_SFULL(s)), 1);
       lgp_mbar_init(BAR(B_SEMPTY(s)), 1);
     }
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < LGP_TC_NSB; ++q) {
       lgp_mbar_init(BAR(B_S1FULL(q)), 1);
       lgp_mbar_init(BAR(B_PFULL(q)), 4);
     }
@@ -331,7 +335,8 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
   // TMEM columns: S buffer q (chunk c uses q = c % 4): 64 FP32 columns of S',
   // then P packed FP16 (hi in columns 0..31, lo in 32..63); D2[w][b]: N columns
 #define T_SB(q) (tmem + 64u * (unsigned)(q))
-#define T_D2(w, b) (tmem + 256u + (unsigned)LGP_TC_N * (2u * (unsigned)(w) + (unsigned)(b)))
+#define T_D2(w, b) \
+  (tmem + 64u * LGP_TC_NSB + (unsigned)LGP_TC_N * (2u * (unsigned)(w) + (unsigned)(b)))
 
   if (warp == 0) {
     if (lane == 0) {
@@ -356,9 +361,17 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       TR_FLUSH(0, 1)
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 10) {
     if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
+      // ------------------------------------------------ MMA issuers
+      // One issuing thread per epilogue warpgroup w (warp 1 -> w 0, warp 10 ->
+      // w 1): it owns that warpgroup's S buffers and D2 accumulators, so both
+      // GEMMs of a chunk are issued in order by one thread (TMEM buffer reuse
+      // is then ordered by the tensor pipe) and the two chains never wait on
+      // each other. Descriptors are precomputed: the start-address field is
+      // linear (a K step of 256 B adds 16, a stage adds STAGE_BYTES/16).
+      const int w = warp == 1 ? 0 : 1;
+      const int nloc = (nch - w + 1) >> 1;
       const unsigned idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(TC_CH >> 3) << 17) |
                               ((unsigned)(128 >> 4) << 24);
       const unsigned idesc2 = (1u << 4) | (0u << 7) | (0u << 10) |
@@ -371,63 +384,62 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       // V tiles exactly representable in FP16 (e.g. +-1 probes) need no V_lo term
       const bool v_exact = a.v_inexact != nullptr && *a.v_inexact == 0;
       lgp_mbar_wait(BAR(B_AFULL), 0);
-      int g1 = 0, g2 = 0;
+      int g1 = 0, g2 = 0;  // local chunk cursors of this warpgroup
       TR_DECL
-      while (g2 < nch) {
-        // distance GEMM of chunk g1 into S buffer g1 % 4 (free once the
-        // contraction of chunk g1 - 4 is issued: the tensor pipe is in order)
-#if LGP_TC_PRIO == 2
-        if (g2 < g1 && lgp_mbar_test(BAR(B_PFULL(g2 & 3)), (g2 >> 2) & 1)) goto do_gemm2;
-#endif
-        if (g1 < nch && g1 < g2 + 4 &&
-            lgp_mbar_test(BAR(B_SFULL(g1 % LGP_TC_STAGES)), (g1 / LGP_TC_STAGES) & 1)) {
-          TR_MARK(2)
-          lgp_tc_fence_after();
-          const int s = g1 % LGP_TC_STAGES;
-          const unsigned long long b_hi = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
-          const unsigned long long b_lo = b_hi + (TC_B1_FLOATS * 4 >> 4);
-          const unsigned d = T_SB(g1 & 3);
+      while (g2 < nloc) {
+        if (g1 < nloc && g1 < g2 + TC_NSBW) {
+          const int c = 2 * g1 + w;
+          const int s = c % LGP_TC_STAGES;
+          if (lgp_mbar_test(BAR(B_SFULL(s)), (c / LGP_TC_STAGES) & 1)) {
+            TR_MARK(2)
+            lgp_tc_fence_after();
+            const int q = w + 2 * (g1 % TC_NSBW);
+            const unsigned long long b_hi = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
+            const unsigned long long b_lo = b_hi + (TC_B1_FLOATS * 4 >> 4);
+            const unsigned d = T_SB(q);
 #pragma unroll
-          for (int kk = 0; kk < LGP_TC_KD / 8; ++kk) {
-            const unsigned o = 16u * kk;
-            lgp_mma_tf32_ss(d, a_hi + o, b_hi + o, idesc1, kk > 0);
-            lgp_mma_tf32_ss(d, a_hi + o, b_lo + o, idesc1, 1);
-            lgp_mma_tf32_ss(d, a_lo + o, b_hi + o, idesc1, 1);
+            for (int kk = 0; kk < LGP_TC_KD / 8; ++kk) {
+              const unsigned o = 16u * kk;
+              lgp_mma_tf32_ss(d, a_hi + o, b_hi + o, idesc1, kk > 0);
+              lgp_mma_tf32_ss(d, a_hi + o, b_lo + o, idesc1, 1);
+              lgp_mma_tf32_ss(d, a_lo + o, b_hi + o, idesc1, 1);
+            }
+            lgp_mma_commit(BAR(B_S1FULL(q)));
+            TR_MARK(3)
+            ++g1;
+            continue;
           }
-          lgp_mma_commit(BAR(B_S1FULL(g1 & 3)));
-          TR_MARK(3)
-          ++g1;
-          continue;
         }
-        if (g2 < g1 && lgp_mbar_test(BAR(B_PFULL(g2 & 3)), (g2 >> 2) & 1)) {
-#if LGP_TC_PRIO == 2
-        do_gemm2:
-#endif
-          TR_MARK(4)
-          const int cc = g2;
-          const int w = cc & 1, k = cc >> 1, gi = k / LGP_TC_G, b = gi & 1;
-          const bool first = (k % LGP_TC_G) == 0;
-          const bool last = ((k % LGP_TC_G) == LGP_TC_G - 1) || (cc + 2 >= nch);
-          if (first && gi >= 2) lgp_mbar_wait(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
-          TR_MARK(6)
-          lgp_tc_fence_after();
-          const int s = cc % LGP_TC_STAGES;
-          const unsigned long long v_hi =
-              dv + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4) + (TC_B1_BYTES >> 4);
-          const unsigned long long v_lo = v_hi + (TC_V_HALFS * 2 >> 4);
-          const unsigned d = T_D2(w, b);
-          const unsigned p = T_SB(cc & 3);
+        if (g2 < g1) {
+          const int q = w + 2 * (g2 % TC_NSBW);
+          if (lgp_mbar_test(BAR(B_PFULL(q)), (g2 / TC_NSBW) & 1)) {
+            TR_MARK(4)
+            const int c = 2 * g2 + w;
+            const int k = g2, gi = k / LGP_TC_G, b = gi & 1;
+            const bool first = (k % LGP_TC_G) == 0;
+            const bool last = ((k % LGP_TC_G) == LGP_TC_G - 1) || (k == nloc - 1);
+            if (first && gi >= 2) lgp_mbar_wait(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
+            TR_MARK(6)
+            lgp_tc_fence_after();
+            const int s = c % LGP_TC_STAGES;
+            const unsigned long long v_hi =
+                dv + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4) + (TC_B1_BYTES >> 4);
+            const unsigned long long v_lo = v_hi + (TC_V_HALFS * 2 >> 4);
+            const unsigned d = T_D2(w, b);
+            const unsigned p = T_SB(q);
 #pragma unroll
-          for (int kk = 0; kk < TC_CH / 16; ++kk) {
-            const unsigned o = 16u * kk;
-            lgp_mma_f16_ts(d, p + 8u * kk, v_hi + o, idesc2, (first && kk == 0) ? 0u : 1u);
-            lgp_mma_f16_ts(d, p + 32u + 8u * kk, v_hi + o, idesc2, 1u);
-            if (!v_exact) lgp_mma_f16_ts(d, p + 8u * kk, v_lo + o, idesc2, 1u);
+            for (int kk = 0; kk < TC_CH / 16; ++kk) {
+              const unsigned o = 16u * kk;
+              if ((LGP_TC_ABLATE & 1) && kk > 0) break;
+              lgp_mma_f16_ts(d, p + 8u * kk, v_hi + o, idesc2, (first && kk == 0) ? 0u : 1u);
+              lgp_mma_f16_ts(d, p + 32u + 8u * kk, v_hi + o, idesc2, 1u);
+              if (!v_exact) lgp_mma_f16_ts(d, p + 8u * kk, v_lo + o, idesc2, 1u);
+            }
+            lgp_mma_commit(BAR(B_SEMPTY(s)));
+            if (last) lgp_mma_commit(BAR(B_D2FULL(w, b)));
+            TR_MARK(7)
+            ++g2;
           }
-          lgp_mma_commit(BAR(B_SEMPTY(s)));
-          if (last) lgp_mma_commit(BAR(B_D2FULL(w, b)));
-          TR_MARK(7)
-          ++g2;
         }
       }
       TR_FLUSH(2, 7)
@@ -463,31 +475,48 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
 
     TR_DECL
     for (int k = 0; k < nloc; ++k) {
-      const int c = 2 * k + w;
-      const unsigned sb = T_SB(c & 3) + lanes;
+      const int q = w + 2 * (k % TC_NSBW);
+      const unsigned sb = T_SB(q) + lanes;
       if (lane == 0) { TR_MARK(8) }
-      lgp_mbar_wait(BAR(B_S1FULL(c & 3)), (c >> 2) & 1);
+      lgp_mbar_wait(BAR(B_S1FULL(q)), (k / TC_NSBW) & 1);
       if (lane == 0) { TR_MARK(9) }
       lgp_tc_fence_after();
       unsigned hi[32], lo[32];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         unsigned s[32];
-        lgp_tmem_ld32(sb + 32u * h, s);
-        lgp_tmem_wait_ld();
+        if (LGP_TC_ABLATE & 4) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[i] = __float_as_uint((float)(i + k) * 0.01f);
+        } else {
+          lgp_tmem_ld32(sb + 32u * h, s);
+          lgp_tmem_wait_ld();
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float k0 = lgp_tc_k(fmaxf(__uint_as_float(s[2 * i]), 0.f), a);
-          const float k1 = lgp_tc_k(fmaxf(__uint_as_float(s[2 * i + 1]), 0.f), a);
-          lgp_split_f16x2(k0, k1, hi[16 * h + i], lo[16 * h + i]);
+          if (LGP_TC_ABLATE & 8) {
+            hi[16 * h + i] = s[2 * i] ^ s[2 * i + 1];
+            lo[16 * h + i] = s[2 * i];
+          } else {
+            const float k0 = lgp_tc_k(fmaxf(__uint_as_float(s[2 * i]), 0.f), a);
+            const float k1 = lgp_tc_k(fmaxf(__uint_as_float(s[2 * i + 1]), 0.f), a);
+            lgp_split_f16x2(k0, k1, hi[16 * h + i], lo[16 * h + i]);
+          }
         }
       }
-      lgp_tmem_st32(sb, hi);
-      lgp_tmem_st32(sb + 32u, lo);
+      if (LGP_TC_ABLATE & 2) {
+        unsigned x_ = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x_ ^= hi[i] ^ lo[i];
+        if (x_ == 0x12345u) comb[0] = 1.0;
+      } else {
+        lgp_tmem_st32(sb, hi);
+        lgp_tmem_st32(sb + 32u, lo);
+      }
       lgp_tmem_wait_st();
       lgp_tc_fence_before();
       __syncwarp();
-      if (lane == 0) lgp_mbar_arrive(BAR(B_PFULL(c & 3)));
+      if (lane == 0) lgp_mbar_arrive(BAR(B_PFULL(q)));
       if (lane == 0) { TR_MARK(10) }
       if (k >= 1 && ((k - 1) % LGP_TC_G) == LGP_TC_G - 1) drain((k - 1) / LGP_TC_G);
       if (lane == 0) { TR_MARK(11) }

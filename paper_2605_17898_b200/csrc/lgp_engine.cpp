@@ -244,7 +244,7 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     }
     a.trace = trace;
     prof_begin();
-    launch(ctx, mod->matvec, (unsigned)grid, 1, 320, plan.smem_bytes, &a);
+    launch(ctx, mod->matvec, (unsigned)grid, 1, plan.tune.threads, plan.smem_bytes, &a);
     prof_end();
     if (trace) {
       unsigned long long h[16];

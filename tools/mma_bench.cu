@@ -15,10 +15,12 @@ __global__ void bench(int n_mma, int N, int alt, long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ unsigned tslot;
   __shared__ __align__(8) unsigned long long bar;
+  __shared__ __align__(8) unsigned long long bar2;
   const int warp = threadIdx.x / 32;
   for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((float*)sm)[i] = 0.001f * (i & 7);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"(saddr(&bar2)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
@@ -35,7 +37,7 @@ __global__ void bench(int n_mma, int N, int alt, long long* out) {
     const unsigned long long da = sdesc(saddr(sm), 512), db = sdesc(saddr(sm + 32768), 512);
     long long t0 = clock64();
     for (int i = 0; i < n_mma; ++i) {
-      const unsigned d = tmem + 256u + (alt ? (unsigned)((i & 1) * 64) : 0u);
+      const unsigned d = tmem + 256u + (alt == 1 ? (unsigned)((i & 1) * 64) : 0u);
       const unsigned acc = i > 1;
       if (TS) {
         const unsigned a = tmem + (unsigned)((i & 3) * 8);
@@ -49,6 +51,8 @@ __global__ void bench(int n_mma, int N, int alt, long long* out) {
         else
           asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d), "l"(da + 16 * (i & 1)), "l"(db + 16 * (i & 1)), "r"(idesc), "r"(acc));
       }
+      if (alt >= 2 && (i % alt) == alt - 1)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(&bar2)));
     }
     long long t1 = clock64();
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(&bar)));
@@ -87,6 +91,12 @@ void run(const char* name, int N, int alt) {
 }
 
 int main() {
+  run<1, 1>("TS f16 N16 commit/1", 16, 2 - 1 + 1);
+  run<1, 1>("TS f16 N16 commit/2", 16, 2);
+  run<1, 1>("TS f16 N16 commit/4", 16, 4);
+  run<1, 1>("TS f16 N16 commit/8", 16, 8);
+  run<0, 0>("SS tf32 N64 commit/3", 64, 3);
+  run<0, 0>("SS tf32 N64 commit/6", 64, 6);
   run<0, 0>("SS tf32 M128 K8", 64, 0);
   run<0, 0>("SS tf32 M128 K8", 64, 1);
   run<0, 0>("SS tf32 M128 K8", 128, 0);
