@@ -11,8 +11,8 @@
 // 64-column chunks.
 //
 //   GEMM1 (tcgen05.mma kind::tf32, 3xTF32 split, A and B from SMEM):
-//       S'[128 x 64] = A1 . B1^T with a_i = [c_i, |c_i|^2, 1], b_j = [-2 c_j, 1, |c_j|^2]
-//       so S'_ij = r^2_ij (lengthscale-scaled) lands in TMEM directly.
+//       S'[128 x 64] = A1 . B1^T with a_i = [c_i, |c_i|^2, 1], b_j = [2 c_j, -1, -|c_j|^2]
+//       so S'_ij = -r^2_ij (lengthscale-scaled) lands in TMEM directly.
 //   epilogue (8 warps, SIMT): r^2 -> k (the tree, one MUFU.EX2 per exp) ->
 //       TF32 hi/lo split -> tcgen05.st back into TMEM as the A operand of
 //   GEMM2 (kind::f16, A = P from TMEM as FP16 hi/lo, B = V tile from SMEM as
@@ -498,8 +498,8 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
             hi[16 * h + i] = s[2 * i] ^ s[2 * i + 1];
             lo[16 * h + i] = s[2 * i];
           } else {
-            const float k0 = lgp_tc_k(fmaxf(__uint_as_float(s[2 * i]), 0.f), a);
-            const float k1 = lgp_tc_k(fmaxf(__uint_as_float(s[2 * i + 1]), 0.f), a);
+            const float k0 = lgp_tc_k(fminf(__uint_as_float(s[2 * i]), 0.f), a);
+            const float k1 = lgp_tc_k(fminf(__uint_as_float(s[2 * i + 1]), 0.f), a);
             lgp_split_f16x2(k0, k1, hi[16 * h + i], lo[16 * h + i]);
           }
         }
