@@ -60,8 +60,10 @@
 #define TC_A1_FLOATS (128 * LGP_TC_KD)
 #define TC_B1_FLOATS (TC_CH * LGP_TC_KD)
 #define TC_V_HALFS (LGP_TC_N * TC_CH)
-#define TC_A1_BYTES (2 * TC_A1_FLOATS * 4)
-#define TC_B1_BYTES (2 * TC_B1_FLOATS * 4)
+// row / column operand tiles: [hi | lo | (negated squared norms)] (norms only
+// used when LGP_TC_SNORM: added in the epilogue instead of riding in K)
+#define TC_A1_BYTES (2 * TC_A1_FLOATS * 4 + 128 * 4)
+#define TC_B1_BYTES (2 * TC_B1_FLOATS * 4 + TC_CH * 4)
 #define TC_V_BYTES (2 * TC_V_HALFS * 2)
 #define TC_STAGE_BYTES (TC_B1_BYTES + TC_V_BYTES)
 #define TC_COMB_BYTES (128 * LGP_TC_N * 8)
@@ -254,6 +256,7 @@ extern "C" __global__ void lgp_tc_prep(LgpPrepArgs p, int tile_rows, int is_col)
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n_pad) return;
   double f[LGP_TC_KD];
+  float nrm = 0.f;
 #pragma unroll
   for (int k = 0; k < LGP_TC_KD; ++k) f[k] = 0.0;
   if (i < p.n) {
@@ -261,13 +264,14 @@ extern "C" __global__ void lgp_tc_prep(LgpPrepArgs p, int tile_rows, int is_col)
     const double* xp = p.x + (p.row0 + i) * LGP_D;
 #pragma unroll
     for (int d = 0; d < LGP_D; ++d) x[d] = xp[d];
-    lgp_tc_prep_point(x, p, is_col, f);
+    lgp_tc_prep_point(x, p, is_col, f, &nrm);
   }
   float* base = is_col ? p.fc : p.fr;
   const long long tile = i / tile_rows;
   const int r = (int)(i % tile_rows);
-  float* hi = base + tile * 2 * tile_rows * LGP_TC_KD;
+  float* hi = base + tile * (2 * tile_rows * LGP_TC_KD + tile_rows);
   float* lo = hi + tile_rows * LGP_TC_KD;
+  lo[tile_rows * LGP_TC_KD + r] = nrm;
 #pragma unroll
   for (int k4 = 0; k4 < LGP_TC_KD; k4 += 4) {
     float h[4], l[4];
@@ -342,7 +346,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
     if (lane == 0) {
       // ------------------------------------------------ producer (TMA bulk)
       lgp_mbar_expect_tx(BAR(B_AFULL), TC_A1_BYTES);
-      lgp_bulk_g2s(lgp_saddr(a1s), a.a1 + (size_t)rb * 2 * TC_A1_FLOATS, TC_A1_BYTES, BAR(B_AFULL));
+      lgp_bulk_g2s(lgp_saddr(a1s), a.a1 + (size_t)rb * (TC_A1_BYTES / 4), TC_A1_BYTES, BAR(B_AFULL));
       const unsigned char* vbase = reinterpret_cast<const unsigned char*>(a.v);
       TR_DECL
       for (int c = 0; c < nch; ++c) {
@@ -352,7 +356,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
         TR_MARK(1)
         const unsigned dst = lgp_saddr(stg + (size_t)s * TC_STAGE_BYTES);
         lgp_mbar_expect_tx(BAR(B_SFULL(s)), TC_STAGE_BYTES);
-        lgp_bulk_g2s(dst, a.b1 + (size_t)(tile0 + c) * 2 * TC_B1_FLOATS, TC_B1_BYTES,
+        lgp_bulk_g2s(dst, a.b1 + (size_t)(tile0 + c) * (TC_B1_BYTES / 4), TC_B1_BYTES,
                      BAR(B_SFULL(s)));
         lgp_bulk_g2s(dst + TC_B1_BYTES,
                      vbase + ((size_t)pass * a.n_tiles + tile0 + c) * TC_V_BYTES, TC_V_BYTES,
@@ -455,6 +459,10 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
     double acc[LGP_TC_N];
 #pragma unroll
     for (int i = 0; i < LGP_TC_N; ++i) acc[i] = 0.0;
+#if LGP_TC_SNORM
+    lgp_mbar_wait(BAR(B_AFULL), 0);
+    const float nrow = a1s[2 * TC_A1_FLOATS + row];
+#endif
 
     auto drain = [&](int gi) {
       const int b = gi & 1;
@@ -482,6 +490,12 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       if (lane == 0) { TR_MARK(9) }
       lgp_tc_fence_after();
       unsigned hi[32], lo[32];
+#if LGP_TC_SNORM
+      const int c = 2 * k + w;
+      lgp_mbar_wait(BAR(B_SFULL(c % LGP_TC_STAGES)), (c / LGP_TC_STAGES) & 1);
+      const float4* ncol = reinterpret_cast<const float4*>(
+          stg + (size_t)(c % LGP_TC_STAGES) * TC_STAGE_BYTES + 2 * TC_B1_FLOATS * 4);
+#endif
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         unsigned s[32];
@@ -498,8 +512,19 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
             hi[16 * h + i] = s[2 * i] ^ s[2 * i + 1];
             lo[16 * h + i] = s[2 * i];
           } else {
+#if LGP_TC_SNORM
+            float n0, n1;
+            {
+              const float4 nc = ncol[(32 * h + 2 * i) >> 2];
+              n0 = (i & 1) ? nc.z : nc.x;
+              n1 = (i & 1) ? nc.w : nc.y;
+            }
+            const float k0 = lgp_tc_k(fminf((__uint_as_float(s[2 * i]) + nrow) + n0, 0.f), a);
+            const float k1 = lgp_tc_k(fminf((__uint_as_float(s[2 * i + 1]) + nrow) + n1, 0.f), a);
+#else
             const float k0 = lgp_tc_k(fminf(__uint_as_float(s[2 * i]), 0.f), a);
             const float k1 = lgp_tc_k(fminf(__uint_as_float(s[2 * i + 1]), 0.f), a);
+#endif
             lgp_split_f16x2(k0, k1, hi[16 * h + i], lo[16 * h + i]);
           }
         }

@@ -118,8 +118,8 @@ void MatvecOp::prepare() {
   partial = (double*)ctx->scratch_get(tag + ".part", (size_t)n_seg * n_pass * n_rows_pad * tb * 8);
   if (plan.tc) {
     // operands pre-tiled in the UMMA canonical layout, TF32 hi/lo split
-    fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * 2 * plan.tc_kd * 4);
-    fc = (float*)ctx->scratch_get(tag + ".b1", (size_t)n_cols_pad * 2 * plan.tc_kd * 4);
+    fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * (2 * plan.tc_kd + 1) * 4);
+    fc = (float*)ctx->scratch_get(tag + ".b1", (size_t)n_cols_pad * (2 * plan.tc_kd + 1) * 4);
     vtc = ctx->scratch_get(tag + ".vtc", (size_t)n_pass * n_cols_pad * 2 * tb * 2);
     vscale = (float*)ctx->scratch_get(tag + ".vscale", (size_t)n_pass * tb * 4);
     v_inexact = (int*)ctx->scratch_get(tag + ".vflag", 16);
