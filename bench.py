@@ -357,6 +357,22 @@ def run_ours(args, rank, world):
                             / (SFU_PER_SM * SM_COUNT * f_mhz * 1e6)}
     if clk.get("sm_mhz"):
         roofline["frac_at_observed_clock"] = achieved / (fp32_peak * clk["sm_mhz"] / f_mhz)
+    if tc:
+        # The tcgen05 kernel does the 2t-flop contraction and the distance cross
+        # term on the tensor cores, so the FP32-SIMT-equivalent rate exceeds the
+        # SIMT FP32 peak. Its binding resources are the MUFU.EX2 pipe (one exp
+        # per entry, sfu_frac) and the tcgen05 instruction rate: measured ~46
+        # cycles per M128 MMA with N <= 64 (tools/mma_bench*.cu), 14 MMAs per
+        # 128x64 entry chunk (6 distance + 8 contraction, +4 when V is not
+        # FP16-exact).
+        chunks = -(-rows_local // 128) * -(-n // 64) * -(-t // 16)
+        mma_cycles = chunks / SM_COUNT * 14 * 46
+        t_issue = mma_cycles / (f_mhz * 1e6)
+        roofline["note"] = ("frac > 1: FP32-equivalent algorithmic rate of a tensor-core kernel; "
+                            "binding resources are MUFU (sfu_frac) and tcgen05 issue "
+                            "(tensor_issue_frac)")
+        roofline["tensor_issue_bound_ms"] = t_issue * 1e3
+        roofline["tensor_issue_frac"] = t_issue / (k1_avg_ms * 1e-3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
