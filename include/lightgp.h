@@ -76,6 +76,7 @@ extern "C" {
 #define LGP_DIST_DIRECT 4u   /* matvec: direct differences instead of the norm trick */
 #define LGP_FORCE_SIMT 8u    /* matvec: never use the tensor-core (tcgen05) kernel */
 #define LGP_NO_SYM 16u       /* matvec: no symmetric block-pair kernel for the square operator */
+#define LGP_INPUTS_FINITE 32u /* caller already validated host inputs as finite (skip the scan) */
 
 typedef struct lgp_ctx lgp_ctx;
 typedef struct lgp_kernel lgp_kernel;

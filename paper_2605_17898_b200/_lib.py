@@ -36,6 +36,7 @@ ACC_FP32 = 2
 DIST_DIRECT = 4
 FORCE_SIMT = 8
 NO_SYM = 16
+INPUTS_FINITE = 32
 
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)

@@ -56,8 +56,12 @@ void require(bool ok, int code, const std::string& msg) {
 }
 
 void check_finite(const double* p, size_t n, const char* name) {
-  for (size_t i = 0; i < n; ++i)
-    if (!std::isfinite(p[i])) throw Error(LGP_E_NONFINITE, std::string(name) + " contains NaN or infinite entries");
+  // branch-free scan (vectorises): a double is finite iff its exponent is not all ones
+  const uint64_t* u = reinterpret_cast<const uint64_t*>(p);
+  const uint64_t m = 0x7ff0000000000000ull;
+  uint64_t bad = 0;
+  for (size_t i = 0; i < n; ++i) bad |= (uint64_t)((u[i] & m) == m);
+  if (bad) throw Error(LGP_E_NONFINITE, std::string(name) + " contains NaN or infinite entries");
 }
 
 // Stage a host or device input (n x t) into a device buffer of n_alloc rows.
@@ -430,7 +434,7 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
   require(t >= 1, LGP_E_ARG, "t must be at least 1");
   require(std::isfinite(noise) && noise >= 0.0, LGP_E_ARG, "noise must be finite and nonnegative");
   require(cols->n == 0 || V, LGP_E_ARG, "V is null");
-  if (!(flags & LGP_DEVICE_PTRS)) check_finite(V, (size_t)cols->n * t, "V");
+  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(V, (size_t)cols->n * t, "V");
   std::lock_guard<std::recursive_mutex> g(ctx->mu);
   ctx->activate();
   const bool square = (rows == cols);
@@ -477,7 +481,7 @@ int lgp_cg(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* pts, double nois
   require(std::isfinite(noise) && noise >= 0.0, LGP_E_ARG, "noise must be finite and nonnegative");
   const int64_t n = pts->n;
   require(n >= 1, LGP_E_DIM, "need at least one point");
-  if (!(flags & LGP_DEVICE_PTRS)) check_finite(B, (size_t)n * t, "b");
+  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(B, (size_t)n * t, "b");
   std::lock_guard<std::recursive_mutex> g(ctx->mu);
   ctx->activate();
   const int64_t S = (n + ctx->world - 1) / ctx->world;
@@ -500,7 +504,7 @@ int lgp_lanczos(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* pts, double
   const int64_t n = pts->n;
   require(n >= 1, LGP_E_DIM, "need at least one point");
   require(steps <= n, LGP_E_ARG, "steps must not exceed n");
-  if (!(flags & LGP_DEVICE_PTRS)) check_finite(Z, (size_t)n * t, "z");
+  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(Z, (size_t)n * t, "z");
   std::lock_guard<std::recursive_mutex> g(ctx->mu);
   ctx->activate();
   const int64_t S = (n + ctx->world - 1) / ctx->world;

@@ -79,9 +79,10 @@ class KernelOperator:
         t = 1 if v.ndim == 1 else v.shape[1]
         out = np.empty(v.shape)
         if self.n and t:
+            # v was validated by as_block above
             _lib.check(_lib.lib().lgp_matvec(self.ctx.handle, self.prog.handle, self.points.handle,
                                              self.points.handle, self.noise, _lib.vptr(v), t,
-                                             _lib.vptr(out), 0))
+                                             _lib.vptr(out), _lib.INPUTS_FINITE))
         return tracked(out)
 
     __call__ = matvec
@@ -95,7 +96,8 @@ class KernelOperator:
         mi = 0 if max_iter is None else int(max_iter)
         _lib.check(_lib.lib().lgp_cg(self.ctx.handle, self.prog.handle, self.points.handle,
                                      self.noise, _lib.vptr(b), t, float(rel_tol), mi,
-                                     _lib.vptr(x), _lib.iptr(iters), _lib.dptr(res), 0))
+                                     _lib.vptr(x), _lib.iptr(iters), _lib.dptr(res),
+                                     _lib.INPUTS_FINITE))
         return x, iters, res
 
     def lanczos(self, z, steps):
@@ -107,7 +109,7 @@ class KernelOperator:
         _lib.check(_lib.lib().lgp_lanczos(self.ctx.handle, self.prog.handle, self.points.handle,
                                           self.noise, _lib.vptr(z), t, int(steps),
                                           _lib.dptr(alphas), _lib.dptr(betas),
-                                          _lib.iptr(counts), 0))
+                                          _lib.iptr(counts), _lib.INPUTS_FINITE))
         return alphas, betas, counts
 
 
