@@ -3,21 +3,24 @@
 // Sum, Product), D >= 4.
 //
 // Prepended by lgp_codegen.cpp: lgp_jit_abi.h, #defines LGP_D, LGP_TC_KD
-// (augmented K of the distance GEMM, multiple of 8), LGP_TC_N (RHS per pass,
-// 16 or 32), LGP_TC_G (chunks per FP32 accumulation group), LGP_TC_STAGES, and
-// the generated lgp_tc_prep_point() / lgp_tc_k().
+// (K of the distance GEMM in FP16 halves: 3D + 4 rounded up to 16), LGP_TC_N
+// (RHS per pass, 16), LGP_TC_G (chunks per FP32 accumulation group),
+// LGP_TC_STAGES, and the generated lgp_tc_prep_point() / lgp_tc_k().
 //
 // Per CTA: 128 rows (one TMEM lane each) x one column segment, streamed in
 // 64-column chunks.
 //
-//   GEMM1 (tcgen05.mma kind::tf32, 3xTF32 split, A and B from SMEM):
-//       S'[128 x 64] = A1 . B1^T with a_i = [c_i, |c_i|^2, 1], b_j = [2 c_j, -1, -|c_j|^2]
-//       so S'_ij = -r^2_ij (lengthscale-scaled) lands in TMEM directly.
+//   GEMM1 (tcgen05.mma kind::f16, A and B from SMEM, FP32 accumulate):
+//       S'[128 x 64] = A1 . B1^T with the FP16 hi/lo split of the augmented
+//       features laid side by side in K (3D + 4 halves, see lgp_tc_prep):
+//       a_i = [c_hi | c_hi | c_lo | n_hi n_lo 1 1], b_j = [2c_hi | 2c_lo | 2c_hi | -1 -1 -m_hi -m_lo]
+//       so S'_ij = 2 c_i.c_j - |c_i|^2 - |c_j|^2 = -r^2_ij (lengthscale-scaled)
+//       lands in TMEM directly: ceil((3D+4)/16) MMAs per chunk (2 for D <= 9).
 //   epilogue (8 warps, SIMT): r^2 -> k (the tree, one MUFU.EX2 per exp) ->
-//       TF32 hi/lo split -> tcgen05.st back into TMEM as the A operand of
-//   GEMM2 (kind::f16, A = P from TMEM as FP16 hi/lo, B = V tile from SMEM as
-//       FP16 hi/lo of a power-of-two column scaling, FP32 accumulate):
-//       D2[128 x N] += P_hi.V_hi + P_lo.V_hi (+ P_hi.V_lo unless V is exact)
+//       FP16 hi/lo split -> tcgen05.st back into TMEM as the A operand of
+//   GEMM2 (kind::f16, A = P from TMEM as FP16 hi/lo, B = [V_hi ; V_lo] tile
+//       from SMEM, FP16 hi/lo of a power-of-two column scaling, N = 2 x RHS):
+//       D2[128 x 2N] += P_hi.[V_hi V_lo] + P_lo.[V_hi V_lo]  (2 MMAs per 16 columns)
 //   D2 (FP32, TMEM) is drained every LGP_TC_G chunks of a warpgroup into FP64
 //   registers; the two epilogue warpgroups' FP64 sums are combined in a fixed
 //   order and written as this segment's partial (deterministic).
@@ -57,13 +60,14 @@
 
 #define TC_CH 64
 #define TC_THREADS 352  // 11 warps: producer, 2 MMA issuers, 2 epilogue warpgroups
-#define TC_A1_FLOATS (128 * LGP_TC_KD)
-#define TC_B1_FLOATS (TC_CH * LGP_TC_KD)
+#if LGP_TC_N != 16
+#error "K1-TC is specialised for 16 RHS per pass"
+#endif
+#define TC_N2 (2 * LGP_TC_N)  // GEMM2 N: V_hi and V_lo rows side by side
 #define TC_V_HALFS (LGP_TC_N * TC_CH)
-// row / column operand tiles: [hi | lo | (negated squared norms)] (norms only
-// used when LGP_TC_SNORM: added in the epilogue instead of riding in K)
-#define TC_A1_BYTES (2 * TC_A1_FLOATS * 4 + 128 * 4)
-#define TC_B1_BYTES (2 * TC_B1_FLOATS * 4 + TC_CH * 4)
+// row / column operand tiles (FP16, UMMA K-major canonical layout)
+#define TC_A1_BYTES (128 * LGP_TC_KD * 2)
+#define TC_B1_BYTES (TC_CH * LGP_TC_KD * 2)
 #define TC_V_BYTES (2 * TC_V_HALFS * 2)
 #define TC_STAGE_BYTES (TC_B1_BYTES + TC_V_BYTES)
 #define TC_COMB_BYTES (128 * LGP_TC_N * 8)
@@ -71,6 +75,9 @@
 #define LGP_TC_NSB 6   // S buffers in TMEM (64 columns each), even: NSB/2 per warpgroup
 #endif
 #define TC_NSBW (LGP_TC_NSB / 2)
+#if 64 * LGP_TC_NSB + 4 * TC_N2 > 512
+#error "TMEM budget: S buffers + 2x2 D2 accumulators exceed 512 columns"
+#endif
 #define TC_NBARS (9 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB)
 
 // barrier slots
@@ -159,12 +166,12 @@ __device__ __forceinline__ unsigned long long lgp_sdesc(unsigned saddr, unsigned
          ((unsigned long long)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-__device__ __forceinline__ void lgp_mma_tf32_ss(unsigned d, unsigned long long ad,
-                                                unsigned long long bd, unsigned idesc,
-                                                unsigned acc) {
+__device__ __forceinline__ void lgp_mma_f16_ss(unsigned d, unsigned long long ad,
+                                               unsigned long long bd, unsigned idesc,
+                                               unsigned acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
 
@@ -238,48 +245,68 @@ __device__ __forceinline__ void lgp_split_f16x2(float x0, float x1, unsigned& hi
   lo = l;
 }
 
-// offset (floats) of element (row r, k) in a K-major no-swizzle TF32 tile with
-// KD columns: 8-row core-matrix groups of (KD/4) x 128 B, K chunks 128 B apart
-__device__ __forceinline__ int lgp_tc_off(int r, int k, int kd) {
-  return (r >> 3) * (kd * 8) + (k >> 2) * 32 + (r & 7) * 4 + (k & 3);
+// offset (halves) of element (row r, k) in a K-major no-swizzle FP16 tile with
+// KH columns: 8-row core-matrix groups of (KH/8) x 128 B, K chunks 128 B apart
+__device__ __forceinline__ int lgp_tc_off(int r, int k, int kh) {
+  return (r >> 3) * (kh * 8) + (k >> 3) * 64 + (r & 7) * 8 + (k & 7);
 }
 
-__device__ __forceinline__ void lgp_tf32_split(double v, float& hi, float& lo) {
-  const float f = (float)v;
-  hi = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
-  lo = (float)(v - (double)hi);
+// FP16 hi/lo split of an FP64 value (round to nearest both times)
+__device__ __forceinline__ void lgp_f16_split(double v, unsigned short& hi, unsigned short& lo) {
+  unsigned short h, l;
+  double hd;
+  asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h) : "d"(v));
+  asm("cvt.f64.f16 %0, %1;" : "=d"(hd) : "h"(h));
+  asm("cvt.rn.f16.f64 %0, %1;" : "=h"(l) : "d"(v - hd));
+  hi = h;
+  lo = l;
 }
 
 // ------------------------------------------------------------ features
-// rows (tile_rows = 128, fr = A1) and columns (tile_rows = 64, fc = B1)
+// rows (tile_rows = 128, fr = A1) and columns (tile_rows = 64, fc = B1): the
+// FP16 hi/lo augmented features, side by side in K (see the header comment).
+// c = lengthscale-scaled centred coordinates; |c| stays far inside the FP16
+// range because wide point sets are routed to the direct-distance kernel
+// (MatvecOp::prepare), and tiny |c| only lose absolute precision below 2^-24.
 extern "C" __global__ void lgp_tc_prep(LgpPrepArgs p, int tile_rows, int is_col) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n_pad) return;
-  double f[LGP_TC_KD];
-  float nrm = 0.f;
+  unsigned short h[LGP_TC_KD];
 #pragma unroll
-  for (int k = 0; k < LGP_TC_KD; ++k) f[k] = 0.0;
+  for (int k = 0; k < LGP_TC_KD; ++k) h[k] = 0;
   if (i < p.n) {
-    double x[LGP_D];
+    double x[LGP_D], c[LGP_D], nn;
     const double* xp = p.x + (p.row0 + i) * LGP_D;
 #pragma unroll
     for (int d = 0; d < LGP_D; ++d) x[d] = xp[d];
-    lgp_tc_prep_point(x, p, is_col, f, &nrm);
+    lgp_tc_prep_point(x, p, c, &nn);
+    unsigned short nh, nl;
+    lgp_f16_split(nn, nh, nl);
+#pragma unroll
+    for (int d = 0; d < LGP_D; ++d) {
+      unsigned short ch, cl;
+      lgp_f16_split(is_col ? 2.0 * c[d] : c[d], ch, cl);
+      h[d] = ch;
+      h[LGP_D + d] = is_col ? cl : ch;
+      h[2 * LGP_D + d] = is_col ? ch : cl;
+    }
+    const unsigned short one = 0x3C00u, sign = 0x8000u;
+    h[3 * LGP_D + 0] = is_col ? (unsigned short)(one | sign) : nh;
+    h[3 * LGP_D + 1] = is_col ? (unsigned short)(one | sign) : nl;
+    h[3 * LGP_D + 2] = is_col ? (unsigned short)(nh ^ sign) : one;
+    h[3 * LGP_D + 3] = is_col ? (unsigned short)(nl ^ sign) : one;
   }
-  float* base = is_col ? p.fc : p.fr;
-  const long long tile = i / tile_rows;
+  unsigned short* base = reinterpret_cast<unsigned short*>(is_col ? p.fc : p.fr) +
+                         (i / tile_rows) * (long long)tile_rows * LGP_TC_KD;
   const int r = (int)(i % tile_rows);
-  float* hi = base + tile * (2 * tile_rows * LGP_TC_KD + tile_rows);
-  float* lo = hi + tile_rows * LGP_TC_KD;
-  lo[tile_rows * LGP_TC_KD + r] = nrm;
 #pragma unroll
-  for (int k4 = 0; k4 < LGP_TC_KD; k4 += 4) {
-    float h[4], l[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) lgp_tf32_split(f[k4 + q], h[q], l[q]);
-    const int o = lgp_tc_off(r, k4, LGP_TC_KD);
-    *reinterpret_cast<float4*>(hi + o) = make_float4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<float4*>(lo + o) = make_float4(l[0], l[1], l[2], l[3]);
+  for (int k8 = 0; k8 < LGP_TC_KD; k8 += 8) {
+    uint4 q;
+    q.x = (unsigned)h[k8 + 0] | ((unsigned)h[k8 + 1] << 16);
+    q.y = (unsigned)h[k8 + 2] | ((unsigned)h[k8 + 3] << 16);
+    q.z = (unsigned)h[k8 + 4] | ((unsigned)h[k8 + 5] << 16);
+    q.w = (unsigned)h[k8 + 6] | ((unsigned)h[k8 + 7] << 16);
+    *reinterpret_cast<uint4*>(base + lgp_tc_off(r, k8, LGP_TC_KD)) = q;
   }
 }
 
@@ -336,11 +363,11 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
   __syncthreads();
   lgp_tc_fence_after();
   const unsigned tmem = *tslot;
-  // TMEM columns: S buffer q (chunk c uses q = c % 4): 64 FP32 columns of S',
-  // then P packed FP16 (hi in columns 0..31, lo in 32..63); D2[w][b]: N columns
+  // TMEM columns: S buffer q: 64 FP32 columns of S', then P packed FP16 (hi in
+  // columns 0..31, lo in 32..63); D2[w][b]: 2N columns (P.V_hi | P.V_lo)
 #define T_SB(q) (tmem + 64u * (unsigned)(q))
 #define T_D2(w, b) \
-  (tmem + 64u * LGP_TC_NSB + (unsigned)LGP_TC_N * (2u * (unsigned)(w) + (unsigned)(b)))
+  (tmem + 64u * LGP_TC_NSB + (unsigned)TC_N2 * (2u * (unsigned)(w) + (unsigned)(b)))
 
   if (warp == 0) {
     if (lane == 0) {
@@ -376,17 +403,13 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       // linear (a K step of 256 B adds 16, a stage adds STAGE_BYTES/16).
       const int w = warp == 1 ? 0 : 1;
       const int nloc = (nch - w + 1) >> 1;
-      const unsigned idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(TC_CH >> 3) << 17) |
-                              ((unsigned)(128 >> 4) << 24);
-      const unsigned idesc2 = (1u << 4) | (0u << 7) | (0u << 10) |
-                              ((unsigned)(LGP_TC_N >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
-      const unsigned long long dk = lgp_sdesc(0u, LGP_TC_KD * 32);
+      // instruction descriptors: FP32 accumulate, FP16 A and B, K-major, M = 128
+      const unsigned idesc1 = (1u << 4) | ((unsigned)(TC_CH >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
+      const unsigned idesc2 = (1u << 4) | ((unsigned)(TC_N2 >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
+      const unsigned long long dk = lgp_sdesc(0u, LGP_TC_KD * 16);
       const unsigned long long dv = lgp_sdesc(0u, 1024u);
-      const unsigned long long a_hi = dk + (lgp_saddr(a1s) >> 4);
-      const unsigned long long a_lo = a_hi + (TC_A1_FLOATS * 4 >> 4);
+      const unsigned long long a_d = dk + (lgp_saddr(a1s) >> 4);
       const unsigned stg0 = lgp_saddr(stg) >> 4;
-      // V tiles exactly representable in FP16 (e.g. +-1 probes) need no V_lo term
-      const bool v_exact = a.v_inexact != nullptr && *a.v_inexact == 0;
       lgp_mbar_wait(BAR(B_AFULL), 0);
       int g1 = 0, g2 = 0;  // local chunk cursors of this warpgroup
       TR_DECL
@@ -398,16 +421,11 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
             TR_MARK(2)
             lgp_tc_fence_after();
             const int q = w + 2 * (g1 % TC_NSBW);
-            const unsigned long long b_hi = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
-            const unsigned long long b_lo = b_hi + (TC_B1_FLOATS * 4 >> 4);
+            const unsigned long long b_d = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
             const unsigned d = T_SB(q);
 #pragma unroll
-            for (int kk = 0; kk < LGP_TC_KD / 8; ++kk) {
-              const unsigned o = 16u * kk;
-              lgp_mma_tf32_ss(d, a_hi + o, b_hi + o, idesc1, kk > 0);
-              lgp_mma_tf32_ss(d, a_hi + o, b_lo + o, idesc1, 1);
-              lgp_mma_tf32_ss(d, a_lo + o, b_hi + o, idesc1, 1);
-            }
+            for (int kk = 0; kk < LGP_TC_KD / 16; ++kk)
+              lgp_mma_f16_ss(d, a_d + 16u * kk, b_d + 16u * kk, idesc1, kk > 0);
             lgp_mma_commit(BAR(B_S1FULL(q)));
             TR_MARK(3)
             ++g1;
@@ -426,18 +444,17 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
             TR_MARK(6)
             lgp_tc_fence_after();
             const int s = c % LGP_TC_STAGES;
-            const unsigned long long v_hi =
+            // B = [V_hi ; V_lo]: the lo rows follow the hi rows in the same layout
+            const unsigned long long v_d =
                 dv + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4) + (TC_B1_BYTES >> 4);
-            const unsigned long long v_lo = v_hi + (TC_V_HALFS * 2 >> 4);
             const unsigned d = T_D2(w, b);
             const unsigned p = T_SB(q);
 #pragma unroll
             for (int kk = 0; kk < TC_CH / 16; ++kk) {
               const unsigned o = 16u * kk;
               if ((LGP_TC_ABLATE & 1) && kk > 0) break;
-              lgp_mma_f16_ts(d, p + 8u * kk, v_hi + o, idesc2, (first && kk == 0) ? 0u : 1u);
-              lgp_mma_f16_ts(d, p + 32u + 8u * kk, v_hi + o, idesc2, 1u);
-              if (!v_exact) lgp_mma_f16_ts(d, p + 8u * kk, v_lo + o, idesc2, 1u);
+              lgp_mma_f16_ts(d, p + 8u * kk, v_d + o, idesc2, (first && kk == 0) ? 0u : 1u);
+              lgp_mma_f16_ts(d, p + 32u + 8u * kk, v_d + o, idesc2, 1u);
             }
             lgp_mma_commit(BAR(B_SEMPTY(s)));
             if (last) lgp_mma_commit(BAR(B_D2FULL(w, b)));
@@ -459,22 +476,19 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
     double acc[LGP_TC_N];
 #pragma unroll
     for (int i = 0; i < LGP_TC_N; ++i) acc[i] = 0.0;
-#if LGP_TC_SNORM
-    lgp_mbar_wait(BAR(B_AFULL), 0);
-    const float nrow = a1s[2 * TC_A1_FLOATS + row];
-#endif
 
     auto drain = [&](int gi) {
       const int b = gi & 1;
       lgp_mbar_wait(BAR(B_D2FULL(w, b)), (gi >> 1) & 1);
       lgp_tc_fence_after();
+      // columns 0..N-1: P.V_hi, N..2N-1: P.V_lo
 #pragma unroll
-      for (int h = 0; h < LGP_TC_N / 16; ++h) {
+      for (int h = 0; h < 2; ++h) {
         unsigned v[16];
         lgp_tmem_ld16(T_D2(w, b) + lanes + 16u * h, v);
         lgp_tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[16 * h + i] += (double)__uint_as_float(v[i]);
+        for (int i = 0; i < 16; ++i) acc[i] += (double)__uint_as_float(v[i]);
       }
       lgp_tc_fence_before();
       __syncwarp();
@@ -490,12 +504,6 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       if (lane == 0) { TR_MARK(9) }
       lgp_tc_fence_after();
       unsigned hi[32], lo[32];
-#if LGP_TC_SNORM
-      const int c = 2 * k + w;
-      lgp_mbar_wait(BAR(B_SFULL(c % LGP_TC_STAGES)), (c / LGP_TC_STAGES) & 1);
-      const float4* ncol = reinterpret_cast<const float4*>(
-          stg + (size_t)(c % LGP_TC_STAGES) * TC_STAGE_BYTES + 2 * TC_B1_FLOATS * 4);
-#endif
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         unsigned s[32];
@@ -512,19 +520,8 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
             hi[16 * h + i] = s[2 * i] ^ s[2 * i + 1];
             lo[16 * h + i] = s[2 * i];
           } else {
-#if LGP_TC_SNORM
-            float n0, n1;
-            {
-              const float4 nc = ncol[(32 * h + 2 * i) >> 2];
-              n0 = (i & 1) ? nc.z : nc.x;
-              n1 = (i & 1) ? nc.w : nc.y;
-            }
-            const float k0 = lgp_tc_k(fminf((__uint_as_float(s[2 * i]) + nrow) + n0, 0.f), a);
-            const float k1 = lgp_tc_k(fminf((__uint_as_float(s[2 * i + 1]) + nrow) + n1, 0.f), a);
-#else
             const float k0 = lgp_tc_k(fminf(__uint_as_float(s[2 * i]), 0.f), a);
             const float k1 = lgp_tc_k(fminf(__uint_as_float(s[2 * i + 1]), 0.f), a);
-#endif
             lgp_split_f16x2(k0, k1, hi[16 * h + i], lo[16 * h + i]);
           }
         }

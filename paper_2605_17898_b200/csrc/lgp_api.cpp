@@ -400,6 +400,16 @@ int lgp_points_upload(lgp_ctx* ctx, const double* X, int64_t n, int32_t d, lgp_p
     for (int j = 0; j < d; ++j) p->center[j] += X[i * d + j];
   if (n > 0)
     for (int j = 0; j < d; ++j) p->center[j] /= (double)n;
+  double r2max = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double r2 = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double e = X[i * d + j] - p->center[j];
+      r2 += e * e;
+    }
+    r2max = std::max(r2max, r2);
+  }
+  p->radius = std::sqrt(r2max);
   const size_t xbytes = ((size_t)std::max<int64_t>(n, 1) * d * 8 + 255) / 256 * 256;
   p->bytes = xbytes + (size_t)d * 8;
   p->x = (double*)ctx->pool_get(p->bytes);

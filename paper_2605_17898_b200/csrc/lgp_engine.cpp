@@ -81,6 +81,19 @@ void launch(Context* ctx, CUfunction f, unsigned gx, unsigned gy, unsigned bx, s
 
 void MatvecOp::prepare() {
   int tb = pick_tb(t);
+  {
+    // wide point sets: the norm trick's cancellation would cost accuracy
+    double c2 = 0.0;
+    for (int j = 0; j < rows->d; ++j) {
+      const double e = rows->center[j] - cols->center[j];
+      c2 += e * e;
+    }
+    const double reach = rows->radius + cols->radius + std::sqrt(c2);
+    if (r2_gain(k->tree) * reach * reach > kNormTrickReach2) {
+      allow_tc = false;
+      flags |= LGP_DIST_DIRECT;
+    }
+  }
   if (allow_tc) plan = make_tc_plan(k->tree, rows->d, t, flags);
   if (plan.tc) {
     tb = plan.tc_n;
@@ -117,9 +130,9 @@ void MatvecOp::prepare() {
 
   partial = (double*)ctx->scratch_get(tag + ".part", (size_t)n_seg * n_pass * n_rows_pad * tb * 8);
   if (plan.tc) {
-    // operands pre-tiled in the UMMA canonical layout, TF32 hi/lo split
-    fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * (2 * plan.tc_kd + 1) * 4);
-    fc = (float*)ctx->scratch_get(tag + ".b1", (size_t)n_cols_pad * (2 * plan.tc_kd + 1) * 4);
+    // operands pre-tiled in the UMMA canonical layout, FP16 hi/lo split
+    fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * plan.tc_kd * 2);
+    fc = (float*)ctx->scratch_get(tag + ".b1", (size_t)n_cols_pad * plan.tc_kd * 2);
     vtc = ctx->scratch_get(tag + ".vtc", (size_t)n_pass * n_cols_pad * 2 * tb * 2);
     vscale = (float*)ctx->scratch_get(tag + ".vscale", (size_t)n_pass * tb * 4);
     v_inexact = (int*)ctx->scratch_get(tag + ".vflag", 16);

@@ -97,7 +97,7 @@ struct Plan {
   size_t smem_bytes = 0;
   // tensor-core variant (tcgen05 3xTF32): r^2-stationary trees, D >= 4, t >= 8
   bool tc = false;
-  int tc_kd = 0;            // K of the distance GEMM (D + 2, multiple of 8)
+  int tc_kd = 0;            // K of the distance GEMM in FP16 halves (3D + 4, multiple of 16)
   int tc_n = 16;            // RHS per pass (GEMM2 N)
   LgpTcArgs tca{};          // kc[] filled
 };
@@ -106,6 +106,13 @@ Plan make_plan(const Tree& tree, int d, int tb, uint32_t flags);
 // The tensor-core plan for the same tree, or a plan with tc == false when the
 // tree / shape is not eligible (see lgp_codegen.cpp).
 Plan make_tc_plan(const Tree& tree, int d, int t, uint32_t flags);
+// Sensitivity of the tree to its squared distances: sum over r^2 leaves of
+// 1.5 / lengthscale^2 (bounds |dk/d r^2| of RBF, Matern-3/2 and -5/2 leaves).
+double r2_gain(const Tree& tree);
+// The norm-trick distances (|c|^2 + |c'|^2 - 2 c.c', FP32 / FP16x2) lose
+// ~2^-22 (|c| + |c'|)^2 absolutely; point sets whose reach (in lengthscales)
+// exceeds this bound use direct differences instead (MatvecOp::prepare).
+constexpr double kNormTrickReach2 = 210.0;
 
 // A loaded JIT module.
 struct Module {
@@ -173,6 +180,7 @@ struct Points {
   double* ctr = nullptr;      // device d FP64: column mean (centring of features)
   size_t bytes = 0;           // pooled block size
   std::vector<double> center; // host copy of ctr
+  double radius = 0.0;        // max_i |x_i - center| (host, FP64)
 };
 
 // ------------------------------------------------------ communicator

@@ -220,8 +220,9 @@ def test_reference_kernel_objects_are_accepted(gpu_ctx):
     np.testing.assert_array_equal(got, want)
 
 
-# ---- tensor-core K1 (tcgen05, 3xTF32 distance GEMM + FP16 hi/lo contraction)
+# ---- tensor-core K1 (tcgen05, FP16x2 distance GEMM + FP16 hi/lo contraction)
 TC_CASES = [("(rbf 0.5)", 300, 8, 16), ("(rbf 0.5)", 1000, 8, 16), ("(matern52 0.7)", 777, 4, 8),
+            ("(rbf 0.3)", 2000, 8, 16), ("(matern32 0.6)", 1500, 12, 16),
             ("(+ (scale 2.0 (rbf 0.4)) (scale 0.5 (matern32 0.9)))", 2049, 6, 20),
             ("(scale 1.5 (matern32 0.5))", 4096, 8, 16), ("(* (rbf 0.8) (matern52 1.1))", 129, 5, 33)]
 
@@ -266,3 +267,30 @@ def test_tensor_core_cfg4_rows(gpu_ctx):
     out = _mv_flags(cfg["kernel"], x, z, cfg["noise"], 0)
     r0, r1 = (int(a) for a in g["cfg4_rows"])
     assert rel_l2(out[r0:r1], g["cfg4_yz"]) <= TOL
+
+
+@pytest.mark.parametrize("expr,d", [("(rbf 0.1)", 8), ("(matern32 0.08)", 6),
+                                    ("(+ (rbf 0.05) (matern52 2.0))", 4)])
+def test_wide_point_sets_keep_accuracy(gpu_ctx, expr, d):
+    """Point sets spanning many lengthscales would lose the norm trick's
+    precision (|c|^2 + |c'|^2 - 2 c.c' cancels); they must still meet the bar
+    (the engine routes them to direct differences), on the square operator
+    and on a cross product with far-away rows."""
+    rng = np.random.default_rng(d)
+    x = rng.random((1500, d)) * 2.0 + 100.0
+    V = rng.standard_normal((1500, 16))
+    tree = O.parse_tree(expr)
+    for flags in (0, _lib.FORCE_SIMT):
+        got = _mv_flags(expr, x, V, 0.1, flags)
+        assert rel_l2(got, O.matvec(tree, x, 0.1, V)) <= TOL
+    xs = rng.random((300, d)) * 2.0 + 100.5
+    k = G.parse_kernel(expr)
+    ctx = _lib.default_context()
+    prog = G.kernels.program(k)
+    rows, cols = _lib.DevicePoints(ctx, xs), _lib.DevicePoints(ctx, x)
+    v = np.ascontiguousarray(V[:, :4])
+    out = np.empty((300, 4))
+    _lib.check(_lib.lib().lgp_matvec(ctx.handle, prog.handle, rows.handle, cols.handle, 0.0,
+                                     _lib.vptr(v), 4, _lib.vptr(out), 0))
+    want = O.gram(tree, xs, x) @ v
+    assert rel_l2(out, want) <= TOL
