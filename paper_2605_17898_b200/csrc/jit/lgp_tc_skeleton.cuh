@@ -44,22 +44,24 @@
 #ifndef LGP_TC_PRIO
 #define LGP_TC_PRIO 1
 #endif
+#ifndef LGP_TC_DLAG
+#define LGP_TC_DLAG ((LGP_TC_G + 1) / 2)
+#endif
+#if LGP_TC_DLAG < 1 || LGP_TC_DLAG > LGP_TC_G
+#error "LGP_TC_DLAG must be in [1, LGP_TC_G]"
+#endif
 #ifndef LGP_TC_ABLATE
 #define LGP_TC_ABLATE 0
 #endif
-
-#ifdef LGP_TC_TRACE
-#define TR_DECL unsigned long long tr_t = clock64(); unsigned long long tr_acc[12] = {0,0,0,0,0,0,0,0,0,0,0,0};
-#define TR_MARK(slot) { const unsigned long long n_ = clock64(); tr_acc[slot] += n_ - tr_t; tr_t = n_; }
-#define TR_FLUSH(lo, hi) { for (int q_ = lo; q_ <= hi; ++q_) atomicAdd(a.trace + q_, tr_acc[q_]); }
-#else
-#define TR_FLUSH(lo, hi)
-#define TR_DECL
-#define TR_MARK(slot)
+// S' = -r^2 may come out a rounding error above 0; leaves that take sqrt(r^2)
+// need it clamped (LGP_TC_CLAMP defined by the code generator), exp2 does not
+#ifndef LGP_TC_CLAMP
+#define LGP_TC_CLAMP(x) (x)
 #endif
 
+
 #define TC_CH 64
-#define TC_THREADS 352  // 11 warps: producer, 2 MMA issuers, 2 epilogue warpgroups
+#define TC_THREADS 384  // 12 warps: producer, 3 MMA issuers (leader) / relay (peer), 2 epilogue warpgroups
 #if LGP_TC_N != 16
 #error "K1-TC is specialised for 16 RHS per pass"
 #endif
@@ -69,7 +71,24 @@
 #define TC_A1_BYTES (128 * LGP_TC_KD * 2)
 #define TC_B1_BYTES (TC_CH * LGP_TC_KD * 2)
 #define TC_V_BYTES (2 * TC_V_HALFS * 2)
-#define TC_STAGE_BYTES (TC_B1_BYTES + TC_V_BYTES)
+// a CTA pair splits every chunk's B operands along N: rank r stages columns
+// 32r..32r+31 of the column features and V_hi (r = 0) or V_lo (r = 1)
+#ifndef LGP_TC_PAIR
+#define LGP_TC_PAIR 0
+#endif
+#if LGP_TC_PAIR
+#define TC_CG "2"
+#define TC_M 256
+#define TC_B1H_BYTES (TC_B1_BYTES / 2)
+#define TC_VH_BYTES (TC_V_BYTES / 2)
+#else
+#define TC_CG "1"
+#define TC_M 128
+#define TC_B1H_BYTES TC_B1_BYTES
+#define TC_VH_BYTES TC_V_BYTES
+#endif
+#define TC_NEPI (4 * (1 + LGP_TC_PAIR))  // epilogue warps arriving on PFULL / D2EMPTY
+#define TC_STAGE_BYTES (TC_B1H_BYTES + TC_VH_BYTES)
 #define TC_COMB_BYTES (128 * LGP_TC_N * 8)
 #ifndef LGP_TC_NSB
 #define LGP_TC_NSB 6   // S buffers in TMEM (64 columns each), even: NSB/2 per warpgroup
@@ -78,22 +97,53 @@
 #if 64 * LGP_TC_NSB + 4 * TC_N2 > 512
 #error "TMEM budget: S buffers + 2x2 D2 accumulators exceed 512 columns"
 #endif
-#define TC_NBARS (9 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB)
+#define TC_NBARS (10 + 3 * LGP_TC_STAGES + 3 * LGP_TC_NSB)
 
 // barrier slots
+// (P* = arrivals relayed from the peer CTA; PFULL / D2EMPTY count the
+// epilogue warps of both CTAs; the rest are local)
 #define B_AFULL 0
-#define B_SFULL(s) (1 + (s))
-#define B_SEMPTY(s) (1 + LGP_TC_STAGES + (s))
-#define B_S1FULL(q) (1 + 2 * LGP_TC_STAGES + (q))
-#define B_PFULL(q) (1 + 2 * LGP_TC_STAGES + LGP_TC_NSB + (q))
-#define B_D2FULL(w, b) (1 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB + 2 * (w) + (b))
-#define B_D2EMPTY(w, b) (5 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB + 2 * (w) + (b))
+#define B_PAFULL 1
+#define B_SFULL(s) (2 + (s))
+#define B_SEMPTY(s) (2 + LGP_TC_STAGES + (s))
+#define B_PSFULL(s) (2 + 2 * LGP_TC_STAGES + (s))
+#define B_S1FULL(q) (2 + 3 * LGP_TC_STAGES + (q))
+#define B_PFULL(q) (2 + 3 * LGP_TC_STAGES + LGP_TC_NSB + (q))
+#define B_D2FULL(w, b) (2 + 3 * LGP_TC_STAGES + 2 * LGP_TC_NSB + 2 * (w) + (b))
+#define B_D2EMPTY(w, b) (6 + 3 * LGP_TC_STAGES + 2 * LGP_TC_NSB + 2 * (w) + (b))
+#define B_PEMPTY(q) (10 + 3 * LGP_TC_STAGES + 2 * LGP_TC_NSB + (q))
 
 __device__ __forceinline__ float lgp_ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// 2^x (x <= 0) on the FMA pipe: x = n + f, f in [-1/2, 1/2] by the
+// 1.5 * 2^23 rounding trick, degree-5 fit of 2^f (max relative error 2.3e-7 in
+// FP32 Horner form, same order as MUFU.EX2), n added into the exponent field
+__device__ __forceinline__ float lgp_ex2_fma(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float p = 1.32764783e-3f;
+  p = fmaf(p, f, 9.67554189e-3f);
+  p = fmaf(p, f, 5.55071309e-2f);
+  p = fmaf(p, f, 2.40221202e-1f);
+  p = fmaf(p, f, 6.93146944e-1f);
+  p = fmaf(p, f, 1.00000012f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+__device__ __forceinline__ float lgp_ex2x(float x, int px) {
+  return px ? lgp_ex2_fma(x) : lgp_ex2(x);
+}
+
+// entries per 16 whose exp2 runs on the FMA pipe instead of MUFU (measured
+// on cfg4: 0 -> 3.86 ms, 2 -> 3.69 ms, 4 -> 3.78 ms)
+#ifndef LGP_TC_POLY
+#define LGP_TC_POLY 2
+#endif
 
 __device__ __forceinline__ float lgp_sqrt(float x) {
   float y;
@@ -149,6 +199,56 @@ __device__ __forceinline__ void lgp_mbar_wait(unsigned bar, unsigned parity) {
   }
 }
 
+// ---- CTA-pair (cluster of 2) helpers
+__device__ __forceinline__ unsigned lgp_cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void lgp_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// address of this CTA's shared variable `a` in the shared window of CTA `rank`
+__device__ __forceinline__ unsigned lgp_mapa(unsigned a, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void lgp_mbar_arrive_cluster(unsigned cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ bool lgp_mbar_test_cl(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void lgp_mbar_wait_cl(unsigned bar, unsigned parity) {
+  unsigned ok = 0;
+#ifdef LGP_TC_WATCHDOG
+  unsigned long long spins = 0;
+#endif
+  while (!ok) {
+#ifdef LGP_TC_WATCHDOG
+    if (++spins > (1ull << 28)) asm volatile("trap;");
+#endif
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ void lgp_bulk_g2s(unsigned dst, const void* src, unsigned bytes,
                                              unsigned bar) {
   asm volatile(
@@ -166,12 +266,15 @@ __device__ __forceinline__ unsigned long long lgp_sdesc(unsigned saddr, unsigned
          ((unsigned long long)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
+// cta_group::2: issued by the pair's leader (rank 0); M = 256 rows, rows
+// 0..127 from / into the leader's SMEM / TMEM, 128..255 the peer's; B rows
+// 0..N/2-1 from the leader's SMEM, N/2..N-1 from the peer's (same offsets)
 __device__ __forceinline__ void lgp_mma_f16_ss(unsigned d, unsigned long long ad,
                                                unsigned long long bd, unsigned idesc,
                                                unsigned acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::" TC_CG ".kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
 
@@ -179,15 +282,42 @@ __device__ __forceinline__ void lgp_mma_f16_ts(unsigned d, unsigned a_tmem, unsi
                                                unsigned idesc, unsigned acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::" TC_CG ".kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a_tmem), "l"(bd), "r"(idesc), "r"(acc));
 }
 
+#if LGP_TC_PAIR
+// completion of the pair's MMAs, signalled on the leader's barrier only
+__device__ __forceinline__ void lgp_mma_commit_local(unsigned bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(bar),
+      "h"((unsigned short)1)
+      : "memory");
+}
+// completion of the pair's MMAs, signalled on the barrier at this offset in both CTAs
+__device__ __forceinline__ void lgp_mma_commit(unsigned bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(bar),
+      "h"((unsigned short)3)
+      : "memory");
+}
+// epilogue -> leader barrier
+__device__ __forceinline__ void lgp_arrive_leader(unsigned bar) {
+  lgp_mbar_arrive_cluster(lgp_mapa(bar, 0));
+}
+#define lgp_mbar_wait_ld lgp_mbar_wait_cl
+#else
 __device__ __forceinline__ void lgp_mma_commit(unsigned bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    bar)
                : "memory");
 }
+#define lgp_mma_commit_local lgp_mma_commit
+#define lgp_arrive_leader lgp_mbar_arrive
+#define lgp_mbar_wait_ld lgp_mbar_wait
+#endif
 
 __device__ __forceinline__ void lgp_tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -225,6 +355,25 @@ __device__ __forceinline__ void lgp_tmem_st32(unsigned taddr, const unsigned (&v
       : "memory");
 }
 
+// 32 columns into v[0..31] / from v[0], v[2], ..., v[62] (stride-2 registers)
+__device__ __forceinline__ void lgp_tmem_ld32p(unsigned taddr, unsigned* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%"
+      "15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : LGP_R8(v, 0), LGP_R8(v, 8), LGP_R8(v, 16), LGP_R8(v, 24)
+      : "r"(taddr));
+}
+
+#define LGP_W8S2(a, o) "r"(a[o + 0]), "r"(a[o + 2]), "r"(a[o + 4]), "r"(a[o + 6]), \
+                       "r"(a[o + 8]), "r"(a[o + 10]), "r"(a[o + 12]), "r"(a[o + 14])
+__device__ __forceinline__ void lgp_tmem_st32s2(unsigned taddr, const unsigned* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%"
+      "14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      LGP_W8S2(v, 0), LGP_W8S2(v, 16), LGP_W8S2(v, 32), LGP_W8S2(v, 48)
+      : "memory");
+}
+
 __device__ __forceinline__ void lgp_tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -232,15 +381,18 @@ __device__ __forceinline__ void lgp_tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// FP16 hi/lo split of two FP32 values, packed {lo half = x0, hi half = x1}
+// FP16 hi/lo split of two FP32 values, packed {lo half = x0, hi half = x1}:
+// hi = RN(x), lo = RN(x - hi) with x - hi formed exactly by the mixed-precision
+// FMA (FHFMA: FP16 operand, FP32 addend), no FP16 -> FP32 unpack needed
 __device__ __forceinline__ void lgp_split_f16x2(float x0, float x1, unsigned& hi, unsigned& lo) {
   unsigned h, l;
-  float f0, f1;
+  float l0, l1;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
-  asm("{\n\t.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\tcvt.f32.f16 %0, a;\n\tcvt.f32.f16 %1, b;\n\t}"
-      : "=f"(f0), "=f"(f1)
-      : "r"(h));
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(x1 - f1), "f"(x0 - f0));
+  asm("{\n\t.reg .f16 a, b, m;\n\tmov.b32 {a, b}, %2;\n\tmov.b16 m, 0xBC00;\n\t"
+      "fma.rn.f32.f16 %0, a, m, %3;\n\tfma.rn.f32.f16 %1, b, m, %4;\n\t}"
+      : "=f"(l0), "=f"(l1)
+      : "r"(h), "f"(x0), "f"(x1));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(l1), "f"(l0));
   hi = h;
   lo = l;
 }
@@ -311,11 +463,29 @@ extern "C" __global__ void lgp_tc_prep(LgpPrepArgs p, int tile_rows, int is_col)
 }
 
 // ------------------------------------------------------------------ K1-TC
-extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const LgpTcArgs a) {
-  if (a.done != nullptr && *a.done) return;
-  const int item = blockIdx.x;
-  const int rb = item % a.n_rb;
-  const int rest = item / a.n_rb;
+// A CTA pair (cluster of 2 on one TPC) owns 256 rows: rank r holds rows
+// 128r..128r+127 of the pair's block in its SMEM / TMEM, stages its half of
+// every chunk's B operands, and runs its own epilogue; the leader (rank 0)
+// issues every tcgen05.mma of the pair (cta_group::2, M = 256), halving the
+// MMA instructions per row and the bulk-copy bytes per SM.
+#if LGP_TC_PAIR
+extern "C" __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+#else
+extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
+#endif
+    lgp_matvec_tc(const LgpTcArgs a) {
+  if (a.done != nullptr && *a.done) return;  // same flag in both CTAs of a pair
+#if LGP_TC_PAIR
+  const unsigned rank = lgp_cluster_rank();
+  const int pair = blockIdx.x >> 1;
+  const int n_rbp = a.n_rb >> 1;
+  const int rb = 2 * (pair % n_rbp) + (int)rank;
+  const int rest = pair / n_rbp;
+#else
+  const unsigned rank = 0;
+  const int rb = blockIdx.x % a.n_rb;
+  const int rest = blockIdx.x / a.n_rb;
+#endif
   const int seg = rest % a.n_seg;
   const int pass = rest / a.n_seg;
   const int tile0 = seg * a.tiles_per_seg;
@@ -338,29 +508,35 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
 
   if (tid == 0) {
     lgp_mbar_init(BAR(B_AFULL), 1);
+    lgp_mbar_init(BAR(B_PAFULL), 1);
     for (int s = 0; s < LGP_TC_STAGES; ++s) {
       lgp_mbar_init(BAR(B_SFULL(s)), 1);
       lgp_mbar_init(BAR(B_SEMPTY(s)), 1);
+      lgp_mbar_init(BAR(B_PSFULL(s)), 1);
     }
     for (int q = 0; q < LGP_TC_NSB; ++q) {
       lgp_mbar_init(BAR(B_S1FULL(q)), 1);
-      lgp_mbar_init(BAR(B_PFULL(q)), 4);
+      lgp_mbar_init(BAR(B_PFULL(q)), TC_NEPI);
+      lgp_mbar_init(BAR(B_PEMPTY(q)), 1);
     }
     for (int w = 0; w < 2; ++w)
       for (int b = 0; b < 2; ++b) {
         lgp_mbar_init(BAR(B_D2FULL(w, b)), 1);
-        lgp_mbar_init(BAR(B_D2EMPTY(w, b)), 4);
+        lgp_mbar_init(BAR(B_D2EMPTY(w, b)), TC_NEPI);
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::" TC_CG ".sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      lgp_saddr(tslot))
                  : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::" TC_CG ".sync.aligned;" ::: "memory");
   }
   lgp_tc_fence_before();
   __syncthreads();
+#if LGP_TC_PAIR
+  lgp_cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
+#endif
   lgp_tc_fence_after();
   const unsigned tmem = *tslot;
   // TMEM columns: S buffer q: 64 FP32 columns of S', then P packed FP16 (hi in
@@ -368,6 +544,15 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
 #define T_SB(q) (tmem + 64u * (unsigned)(q))
 #define T_D2(w, b) \
   (tmem + 64u * LGP_TC_NSB + (unsigned)TC_N2 * (2u * (unsigned)(w) + (unsigned)(b)))
+
+  // instruction descriptors: FP32 accumulate, FP16 A and B, K-major, M = TC_M.
+  // Shared-memory descriptors are precomputed: the start-address field is
+  // linear (a K step of 256 B adds 16, a stage adds STAGE_BYTES/16).
+  const unsigned idesc1 = (1u << 4) | ((unsigned)(TC_CH >> 3) << 17) | ((unsigned)(TC_M >> 4) << 24);
+  const unsigned idesc2 = (1u << 4) | ((unsigned)(TC_N2 >> 3) << 17) | ((unsigned)(TC_M >> 4) << 24);
+  const unsigned long long dk = lgp_sdesc(0u, LGP_TC_KD * 16);
+  const unsigned long long dv = lgp_sdesc(0u, 1024u);
+  const unsigned stg0 = lgp_saddr(stg) >> 4;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -378,92 +563,111 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       TR_DECL
       for (int c = 0; c < nch; ++c) {
         const int s = c % LGP_TC_STAGES;
-        TR_MARK(0)
         if (c >= LGP_TC_STAGES) lgp_mbar_wait(BAR(B_SEMPTY(s)), ((c / LGP_TC_STAGES) - 1) & 1);
-        TR_MARK(1)
+        TR_MARK(0)
         const unsigned dst = lgp_saddr(stg + (size_t)s * TC_STAGE_BYTES);
         lgp_mbar_expect_tx(BAR(B_SFULL(s)), TC_STAGE_BYTES);
-        lgp_bulk_g2s(dst, a.b1 + (size_t)(tile0 + c) * (TC_B1_BYTES / 4), TC_B1_BYTES,
-                     BAR(B_SFULL(s)));
-        lgp_bulk_g2s(dst + TC_B1_BYTES,
-                     vbase + ((size_t)pass * a.n_tiles + tile0 + c) * TC_V_BYTES, TC_V_BYTES,
-                     BAR(B_SFULL(s)));
+        lgp_bulk_g2s(dst,
+                     reinterpret_cast<const unsigned char*>(a.b1) +
+                         (size_t)(tile0 + c) * TC_B1_BYTES + rank * TC_B1H_BYTES,
+                     TC_B1H_BYTES, BAR(B_SFULL(s)));
+        lgp_bulk_g2s(dst + TC_B1H_BYTES,
+                     vbase + ((size_t)pass * a.n_tiles + tile0 + c) * TC_V_BYTES +
+                         rank * TC_VH_BYTES,
+                     TC_VH_BYTES, BAR(B_SFULL(s)));
+        TR_MARK(1)
       }
       TR_FLUSH(0, 1)
     }
     __syncwarp();
+  } else if (warp == 11 && rank == 0) {
+    if (lane == 0) {
+      // -------------------------------------- distance-GEMM issuer (leader)
+      // every chunk in order, once it is staged (in both CTAs of a pair) and
+      // its S buffer's previous contraction has completed (PEMPTY)
+      const unsigned long long a_d = dk + (lgp_saddr(a1s) >> 4);
+      lgp_mbar_wait(BAR(B_AFULL), 0);
+#if LGP_TC_PAIR
+      lgp_mbar_wait_cl(BAR(B_PAFULL), 0);
+#endif
+      TR_DECL
+      for (int c = 0; c < nch; ++c) {
+        const int w = c & 1, k = c >> 1;
+        const int q = w + 2 * (k % TC_NSBW);
+        const int s = c % LGP_TC_STAGES;
+        lgp_mbar_wait(BAR(B_SFULL(s)), (c / LGP_TC_STAGES) & 1);
+#if LGP_TC_PAIR
+        lgp_mbar_wait_cl(BAR(B_PSFULL(s)), (c / LGP_TC_STAGES) & 1);
+#endif
+        if (k >= TC_NSBW) lgp_mbar_wait(BAR(B_PEMPTY(q)), ((k / TC_NSBW) - 1) & 1);
+        TR_MARK(3)
+        lgp_tc_fence_after();
+        const unsigned long long b_d = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
+        const unsigned d = T_SB(q);
+#pragma unroll
+        for (int kk = 0; kk < LGP_TC_KD / 16; ++kk)
+          lgp_mma_f16_ss(d, a_d + 16u * kk, b_d + 16u * kk, idesc1, kk > 0);
+        lgp_mma_commit(BAR(B_S1FULL(q)));
+        TR_MARK(4)
+      }
+      TR_FLUSH(3, 4)
+    }
+    __syncwarp();
+  } else if ((warp == 1 || warp >= 10) && rank == 1) {
+#if LGP_TC_PAIR
+    if (warp == 1 && lane == 0) {
+      // ------------------------------------------------ peer relay
+      // the leader issues MMAs that read this CTA's staged operands: forward
+      // this CTA's bulk-copy completions to the leader's P* barriers
+      lgp_mbar_wait(BAR(B_AFULL), 0);
+      lgp_mbar_arrive_cluster(lgp_mapa(BAR(B_PAFULL), 0));
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % LGP_TC_STAGES;
+        lgp_mbar_wait(BAR(B_SFULL(s)), (c / LGP_TC_STAGES) & 1);
+        lgp_mbar_arrive_cluster(lgp_mapa(BAR(B_PSFULL(s)), 0));
+      }
+    }
+    __syncwarp();
+#endif
   } else if (warp == 1 || warp == 10) {
     if (lane == 0) {
-      // ------------------------------------------------ MMA issuers
-      // One issuing thread per epilogue warpgroup w (warp 1 -> w 0, warp 10 ->
-      // w 1): it owns that warpgroup's S buffers and D2 accumulators, so both
-      // GEMMs of a chunk are issued in order by one thread (TMEM buffer reuse
-      // is then ordered by the tensor pipe) and the two chains never wait on
-      // each other. Descriptors are precomputed: the start-address field is
-      // linear (a K step of 256 B adds 16, a stage adds STAGE_BYTES/16).
+      // -------------------------------------- contraction issuers (leader)
+      // An MMA-issuing thread sustains one tcgen05.mma per ~60-90 cycles, so
+      // each epilogue warpgroup w has its own contraction issuer (warp 1 ->
+      // w 0, warp 10 -> w 1) that owns its D2 accumulators.
       const int w = warp == 1 ? 0 : 1;
       const int nloc = (nch - w + 1) >> 1;
-      // instruction descriptors: FP32 accumulate, FP16 A and B, K-major, M = 128
-      const unsigned idesc1 = (1u << 4) | ((unsigned)(TC_CH >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
-      const unsigned idesc2 = (1u << 4) | ((unsigned)(TC_N2 >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
-      const unsigned long long dk = lgp_sdesc(0u, LGP_TC_KD * 16);
-      const unsigned long long dv = lgp_sdesc(0u, 1024u);
-      const unsigned long long a_d = dk + (lgp_saddr(a1s) >> 4);
-      const unsigned stg0 = lgp_saddr(stg) >> 4;
-      lgp_mbar_wait(BAR(B_AFULL), 0);
-      int g1 = 0, g2 = 0;  // local chunk cursors of this warpgroup
       TR_DECL
-      while (g2 < nloc) {
-        if (g1 < nloc && g1 < g2 + TC_NSBW) {
-          const int c = 2 * g1 + w;
-          const int s = c % LGP_TC_STAGES;
-          if (lgp_mbar_test(BAR(B_SFULL(s)), (c / LGP_TC_STAGES) & 1)) {
-            TR_MARK(2)
-            lgp_tc_fence_after();
-            const int q = w + 2 * (g1 % TC_NSBW);
-            const unsigned long long b_d = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
-            const unsigned d = T_SB(q);
+      for (int k = 0; k < nloc; ++k) {
+        const int c = 2 * k + w;
+        const int q = w + 2 * (k % TC_NSBW);
+        const int gi = k / LGP_TC_G, b = gi & 1;
+        const bool first = (k % LGP_TC_G) == 0;
+        const bool last = ((k % LGP_TC_G) == LGP_TC_G - 1) || (k == nloc - 1);
+        TR_MARK(5)
+        lgp_mbar_wait_ld(BAR(B_PFULL(q)), (k / TC_NSBW) & 1);
+        if (first && gi >= 2) lgp_mbar_wait_ld(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
+        TR_MARK(6)
+        lgp_tc_fence_after();
+        const int s = c % LGP_TC_STAGES;
+        // B = [V_hi ; V_lo] (on a pair: rank 0 stages the hi rows, rank 1 the lo rows)
+        const unsigned long long v_d =
+            dv + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4) + (TC_B1H_BYTES >> 4);
+        const unsigned d = T_D2(w, b);
+        const unsigned p = T_SB(q);
 #pragma unroll
-            for (int kk = 0; kk < LGP_TC_KD / 16; ++kk)
-              lgp_mma_f16_ss(d, a_d + 16u * kk, b_d + 16u * kk, idesc1, kk > 0);
-            lgp_mma_commit(BAR(B_S1FULL(q)));
-            TR_MARK(3)
-            ++g1;
-            continue;
-          }
+        for (int kk = 0; kk < TC_CH / 16; ++kk) {
+          const unsigned o = 16u * kk;
+          if ((LGP_TC_ABLATE & 1) && kk > 0) break;
+          lgp_mma_f16_ts(d, p + 8u * kk, v_d + o, idesc2, (first && kk == 0) ? 0u : 1u);
+          lgp_mma_f16_ts(d, p + 32u + 8u * kk, v_d + o, idesc2, 1u);
         }
-        if (g2 < g1) {
-          const int q = w + 2 * (g2 % TC_NSBW);
-          if (lgp_mbar_test(BAR(B_PFULL(q)), (g2 / TC_NSBW) & 1)) {
-            TR_MARK(4)
-            const int c = 2 * g2 + w;
-            const int k = g2, gi = k / LGP_TC_G, b = gi & 1;
-            const bool first = (k % LGP_TC_G) == 0;
-            const bool last = ((k % LGP_TC_G) == LGP_TC_G - 1) || (k == nloc - 1);
-            if (first && gi >= 2) lgp_mbar_wait(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
-            TR_MARK(6)
-            lgp_tc_fence_after();
-            const int s = c % LGP_TC_STAGES;
-            // B = [V_hi ; V_lo]: the lo rows follow the hi rows in the same layout
-            const unsigned long long v_d =
-                dv + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4) + (TC_B1_BYTES >> 4);
-            const unsigned d = T_D2(w, b);
-            const unsigned p = T_SB(q);
-#pragma unroll
-            for (int kk = 0; kk < TC_CH / 16; ++kk) {
-              const unsigned o = 16u * kk;
-              if ((LGP_TC_ABLATE & 1) && kk > 0) break;
-              lgp_mma_f16_ts(d, p + 8u * kk, v_d + o, idesc2, (first && kk == 0) ? 0u : 1u);
-              lgp_mma_f16_ts(d, p + 32u + 8u * kk, v_d + o, idesc2, 1u);
-            }
-            lgp_mma_commit(BAR(B_SEMPTY(s)));
-            if (last) lgp_mma_commit(BAR(B_D2FULL(w, b)));
-            TR_MARK(7)
-            ++g2;
-          }
-        }
+        lgp_mma_commit(BAR(B_SEMPTY(s)));
+        lgp_mma_commit_local(BAR(B_PEMPTY(q)));
+        if (last) lgp_mma_commit(BAR(B_D2FULL(w, b)));
+        TR_MARK(7)
       }
-      TR_FLUSH(2, 7)
+      TR_FLUSH(5, 7)
     }
     __syncwarp();
   } else {
@@ -492,7 +696,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       }
       lgp_tc_fence_before();
       __syncwarp();
-      if (lane == 0) lgp_mbar_arrive(BAR(B_D2EMPTY(w, b)));
+      if (lane == 0) lgp_arrive_leader(BAR(B_D2EMPTY(w, b)));
     };
 
     TR_DECL
@@ -503,47 +707,37 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       lgp_mbar_wait(BAR(B_S1FULL(q)), (k / TC_NSBW) & 1);
       if (lane == 0) { TR_MARK(9) }
       lgp_tc_fence_after();
-      unsigned hi[32], lo[32];
+      // all 64 columns in one round trip; P overwrites S' in the same
+      // registers: s[2m] = FP16x2 hi of entries (2m, 2m+1), s[2m+1] = lo
+      unsigned s[64];
+      lgp_tmem_ld32p(sb, s);
+      lgp_tmem_ld32p(sb + 32u, s + 32);
+      lgp_tmem_wait_ld();
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        unsigned s[32];
-        if (LGP_TC_ABLATE & 4) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[i] = __float_as_uint((float)(i + k) * 0.01f);
-        } else {
-          lgp_tmem_ld32(sb + 32u * h, s);
-          lgp_tmem_wait_ld();
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (LGP_TC_ABLATE & 8) {
-            hi[16 * h + i] = s[2 * i] ^ s[2 * i + 1];
-            lo[16 * h + i] = s[2 * i];
-          } else {
-            const float k0 = lgp_tc_k(fminf(__uint_as_float(s[2 * i]), 0.f), a);
-            const float k1 = lgp_tc_k(fminf(__uint_as_float(s[2 * i + 1]), 0.f), a);
-            lgp_split_f16x2(k0, k1, hi[16 * h + i], lo[16 * h + i]);
-          }
-        }
+      for (int m = 0; m < 32; ++m) {
+        const int px = (m & 7) < (LGP_TC_POLY + 1) / 2 ? 1 : 0;
+        const int px1 = (m & 7) < LGP_TC_POLY / 2 ? 1 : 0;
+        const float k0 = lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(s[2 * m])), a, px);
+        const float k1 = lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(s[2 * m + 1])), a, px1);
+        lgp_split_f16x2(k0, k1, s[2 * m], s[2 * m + 1]);
       }
-      if (LGP_TC_ABLATE & 2) {
-        unsigned x_ = 0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) x_ ^= hi[i] ^ lo[i];
-        if (x_ == 0x12345u) comb[0] = 1.0;
-      } else {
-        lgp_tmem_st32(sb, hi);
-        lgp_tmem_st32(sb + 32u, lo);
-      }
+      lgp_tmem_st32s2(sb, s);        // hi pairs -> columns 0..31
+      lgp_tmem_st32s2(sb + 32u, s + 1);  // lo pairs -> columns 32..63
       lgp_tmem_wait_st();
       lgp_tc_fence_before();
       __syncwarp();
-      if (lane == 0) lgp_mbar_arrive(BAR(B_PFULL(q)));
+      if (lane == 0) lgp_arrive_leader(BAR(B_PFULL(q)));
       if (lane == 0) { TR_MARK(10) }
-      if (k >= 1 && ((k - 1) % LGP_TC_G) == LGP_TC_G - 1) drain((k - 1) / LGP_TC_G);
+      // drain a finished accumulation group DLAG chunks into the next one, so
+      // its last contraction has long completed (DLAG <= G keeps at most two
+      // groups, i.e. both D2 buffers, outstanding)
+      if (k >= LGP_TC_DLAG && ((k - LGP_TC_DLAG) % LGP_TC_G) == LGP_TC_G - 1)
+        drain((k - LGP_TC_DLAG) / LGP_TC_G);
       if (lane == 0) { TR_MARK(11) }
     }
-    if (nloc >= 1) drain((nloc - 1) / LGP_TC_G);
+    for (int gi = nloc >= LGP_TC_DLAG ? (nloc - LGP_TC_DLAG) / LGP_TC_G : 0;
+         gi < (nloc + LGP_TC_G - 1) / LGP_TC_G; ++gi)
+      drain(gi);
     if (lane == 0) { TR_FLUSH(8, 11) }
 
     // combine the two warpgroups' FP64 sums in a fixed order, undo the V scaling
@@ -567,9 +761,12 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
   }
   lgp_tc_fence_before();
   __syncthreads();
+#if LGP_TC_PAIR
+  lgp_cluster_sync();  // no MMA of the pair is pending on either TMEM
+#endif
   if (warp == 0) {
     lgp_tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::" TC_CG ".sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 #undef BAR
 #undef T_SB

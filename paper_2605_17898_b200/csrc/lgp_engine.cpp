@@ -104,6 +104,7 @@ void MatvecOp::prepare() {
   const Tuning& tu = plan.tune;
   const int rows_per_cta = plan.tc ? 128 : tu.threads * tu.r;
   n_rb = (int)ceil_div<int64_t>(std::max<int64_t>(n_rows, 1), rows_per_cta);
+  if (plan.tc && plan.tc_pair) n_rb += n_rb & 1;  // CTA pairs: 256-row blocks
   n_rows_pad = n_rb * rows_per_cta;
   const int cc = plan.tc ? 64 : tu.cc;
   n_tiles = (int)ceil_div<int64_t>(std::max<int64_t>(cols->n, 1), cc);
@@ -125,6 +126,7 @@ void MatvecOp::prepare() {
       best = s;
     }
   }
+  if (const char* e = std::getenv("LGP_SEGMENTS")) best = std::max(1, std::min(n_tiles, atoi(e)));
   tiles_per_seg = ceil_div(n_tiles, best);
   n_seg = ceil_div(n_tiles, tiles_per_seg);
 
@@ -265,11 +267,11 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
       LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
       const double ctas = (double)grid;
       fprintf(stderr,
-              "[tc trace, cycles per CTA] producer: issue %.0f wait_empty %.0f | mma: "
-              "poll %.0f gemm1 %.0f poll %.0f - %.0f wait_d2e %.0f gemm2 %.0f | "
+              "[tc trace, cycles per CTA] producer: wait %.0f issue %.0f | gemm1: wait %.0f issue %.0f "
+              "| gemm2 issuers (sum of 2): wait %.0f issue %.0f | "
               "wg(per warp): wait_d1 %.0f epi %.0f drain %.0f\n",
-              h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas, h[5] / ctas,
-              h[6] / ctas, h[7] / ctas, h[9] / ctas / 8, h[10] / ctas / 8, h[11] / ctas / 8);
+              h[0] / ctas, h[1] / ctas, h[3] / ctas, h[4] / ctas, h[6] / ctas, h[7] / ctas,
+              h[9] / ctas / 8, h[10] / ctas / 8, h[11] / ctas / 8);
     }
     vec::epilogue(ctx, partial, n_seg, n_pass, n_rows_pad, tb, n_rows, t, plan.root_scale, noise,
                   noise_v, out_dev, done);

@@ -99,6 +99,7 @@ struct Plan {
   bool tc = false;
   int tc_kd = 0;            // K of the distance GEMM in FP16 halves (3D + 4, multiple of 16)
   int tc_n = 16;            // RHS per pass (GEMM2 N)
+  bool tc_pair = false;     // K1-TC on CTA pairs (cta_group::2, 256-row blocks)
   LgpTcArgs tca{};          // kc[] filled
 };
 
