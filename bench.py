@@ -45,6 +45,7 @@ UNIT = "Gentries/s"
 SM_COUNT = 148
 FP32_LANES = 128
 SFU_PER_SM = 16
+TMEM_LD_B_PER_CLK = 40.8  # measured tcgen05.ld throughput per SM (tools/tmem_bench.cu)
 
 
 def flops_per_entry(kernel_expr, d, t):
@@ -311,6 +312,10 @@ def run_ours(args, rank, world):
     solve = {}
     if not args.no_solve:
         op = G.KernelOperator(kernel, x, cfg["noise"], ctx=ctx)
+        # warm-up: JIT modules / scratch of the t = 1 CG kernels and the SLQ block
+        op.cg(y, 1e-8, 2)
+        op.lanczos(G.probe_block(n, t if t > 1 else 16, 0), 2)
+        ctx.k1_profile(reset=True)
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
@@ -345,34 +350,47 @@ def run_ours(args, rank, world):
     except Exception:
         pass
     tc = "lgp_matvec_tc" in prog.source(d, t)
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": traffic,
-                "kernel": ("lgp_matvec_tc (fused K1, tcgen05 3xTF32 distance GEMM + FP16x2 "
-                           "contraction)" if tc else "lgp_matvec (fused K1, SIMT FP32/FP64)"),
-                "k1_ms_per_launch": k1_avg_ms,
-                "flops_per_entry": flops, "sfu_per_entry": sfu,
-                "peak_source": f"derived: 2 x {FP32_LANES} FP32 lanes x {SM_COUNT} SMs x "
-                               f"{f_mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)",
-                "sfu_frac": rows_local * n * sfu / (k1_avg_ms * 1e-3)
-                            / (SFU_PER_SM * SM_COUNT * f_mhz * 1e6)}
-    if clk.get("sm_mhz"):
-        roofline["frac_at_observed_clock"] = achieved / (fp32_peak * clk["sm_mhz"] / f_mhz)
+    sfu_frac = rows_local * n * sfu / (k1_avg_ms * 1e-3) / (SFU_PER_SM * SM_COUNT * f_mhz * 1e6)
     if tc:
-        # The tcgen05 kernel does the 2t-flop contraction and the distance cross
-        # term on the tensor cores, so the FP32-SIMT-equivalent rate exceeds the
-        # SIMT FP32 peak. Its binding resources are the MUFU.EX2 pipe (one exp
-        # per entry, sfu_frac) and the tcgen05 instruction rate: measured ~46
-        # cycles per M128 MMA with N <= 64 (tools/mma_bench*.cu), 14 MMAs per
-        # 128x64 entry chunk (6 distance + 8 contraction, +4 when V is not
-        # FP16-exact).
-        chunks = -(-rows_local // 128) * -(-n // 64) * -(-t // 16)
-        mma_cycles = chunks / SM_COUNT * 14 * 46
-        t_issue = mma_cycles / (f_mhz * 1e6)
-        roofline["note"] = ("frac > 1: FP32-equivalent algorithmic rate of a tensor-core kernel; "
-                            "binding resources are MUFU (sfu_frac) and tcgen05 issue "
-                            "(tensor_issue_frac)")
-        roofline["tensor_issue_bound_ms"] = t_issue * 1e3
-        roofline["tensor_issue_frac"] = t_issue / (k1_avg_ms * 1e-3)
+        # K1-TC's binding resource is the TMEM -> register path: every kernel
+        # entry's FP32 -r^2 is read once by tcgen05.ld (4 B / entry / pass).
+        # Peak = measured tcgen05.ld throughput, 40.8 B/clk/SM on this B200
+        # (tools/tmem_bench.cu, flat in shape and warp count), x 148 SMs x clock.
+        n_pass = -(-t // 16)
+        tmem_bytes = rows_local * n * 4 * n_pass
+        tmem_peak = TMEM_LD_B_PER_CLK * SM_COUNT * f_mhz * 1e6 / 1e9  # GB/s
+        tmem_ach = tmem_bytes / (k1_avg_ms * 1e-3) / 1e9
+        # tensor-core work: distance GEMM (K = 3D+4 rounded to 16) + contraction
+        # (K = 2 x 64 per chunk, N = 32) over 128 x 64 chunks
+        kh = -(-(3 * d + 4) // 16) * 16
+        chunks = -(-rows_local // 128) * -(-n // 64) * n_pass
+        tflop = chunks * (2 * 128 * 64 * kh + 2 * 128 * 32 * 128) / (k1_avg_ms * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "achieved": tmem_ach, "peak": tmem_peak, "unit": "GB/s",
+                    "frac": tmem_ach / tmem_peak, "traffic": traffic,
+                    "kernel": "lgp_matvec_tc (fused K1: tcgen05 FP16x2 distance GEMM -> TMEM -> "
+                              "exp2 epilogue -> FP16 hi/lo contraction GEMM)",
+                    "k1_ms_per_launch": k1_avg_ms,
+                    "resource": "tensor-memory loads (tcgen05.ld of the FP32 distance tile), "
+                                "4 B per kernel entry",
+                    "peak_source": f"measured tcgen05.ld {TMEM_LD_B_PER_CLK} B/clk/SM "
+                                   f"(tools/tmem_bench.cu) x {SM_COUNT} SMs x {f_mhz:.0f} MHz",
+                    "tensor_tflops": tflop,
+                    "tensor_frac_of_bf16_dense": tflop / float(pk.get("bf16_tflops", 1652.9)),
+                    "sfu_frac": sfu_frac,
+                    "fp32_equivalent_tflops": achieved,
+                    "hbm_frac": (traffic / (k1_avg_ms * 1e-3) / 1e9 / float(pk.get("hbm_gbs", 6449.1))
+                                 if traffic else None)}
+    else:
+        roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp32_peak, "traffic": traffic,
+                    "kernel": "lgp_matvec (fused K1, SIMT FP32/FP64)",
+                    "k1_ms_per_launch": k1_avg_ms,
+                    "flops_per_entry": flops, "sfu_per_entry": sfu,
+                    "peak_source": f"derived: 2 x {FP32_LANES} FP32 lanes x {SM_COUNT} SMs x "
+                                   f"{f_mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)",
+                    "sfu_frac": sfu_frac}
+        if clk.get("sm_mhz"):
+            roofline["frac_at_observed_clock"] = achieved / (fp32_peak * clk["sm_mhz"] / f_mhz)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,

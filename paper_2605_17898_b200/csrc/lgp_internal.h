@@ -260,6 +260,11 @@ void dot_partial(Context* c, const double* a, const double* b, int64_t n, int t,
                  const int* done);
 void dot_final(Context* c, const double* part, int nblk, int t, double* out, const int* done);
 void fill(Context* c, double* p, int64_t n, double v);
+// point-set statistics on the device: ctr[d] = column means (fixed-order
+// reduction); stats[d + 2] = [means | max |x_i - mean|^2 | non-finite flag];
+// scratch >= reduce_blocks(n, 1) * d doubles
+void point_stats(Context* c, const double* x, int64_t n, int d, double* ctr, double* scratch,
+                 double* stats);
 
 // CG (solvers.py:87-123), see lgp_vec.cu
 struct CgState {

@@ -445,6 +445,61 @@ __global__ void k_lz_normalize(const double* __restrict__ w, double* __restrict_
   }
 }
 
+// ---- point-set statistics (lgp_points_upload): column means, finiteness,
+// radius about the mean. Block (b, j) sums column j over row chunk b in a
+// fixed order, so the mean is deterministic (and identical on every rank).
+__global__ void k_pt_colsum(const double* __restrict__ x, long long n, int d, long long rows,
+                            double* __restrict__ part, int* bad) {
+  const int j = blockIdx.y;
+  const long long r0 = (long long)blockIdx.x * rows;
+  long long r1 = r0 + rows;
+  if (r1 > n) r1 = n;
+  double acc = 0.0;
+  int nf = 0;
+  for (long long i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const double v = x[i * d + j];
+    nf |= !isfinite(v);
+    acc += v;
+  }
+  __shared__ double sh[256];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[(long long)blockIdx.x * d + j] = sh[0];
+  if (nf) atomicOr(bad, 1);
+}
+
+__global__ void k_pt_center(const double* __restrict__ part, int nblk, int d, long long n,
+                            double* ctr, double* stats) {
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < nblk; ++b) acc += part[(long long)b * d + j];
+    const double c = n > 0 ? acc / (double)n : 0.0;
+    ctr[j] = c;
+    stats[j] = c;
+  }
+}
+
+__global__ void k_pt_radius(const double* __restrict__ x, long long n, int d,
+                            const double* __restrict__ ctr, unsigned long long* r2max) {
+  double m = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double r2 = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double e = x[i * d + j] - ctr[j];
+      r2 += e * e;
+    }
+    m = fmax(m, r2);
+  }
+  // non-negative doubles order like their bit patterns
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && isfinite(m)) atomicMax(r2max, __double_as_longlong(m));
+}
+
 inline int grid_for(long long total, int bd = 256) {
   long long g = (total + bd - 1) / bd;
   if (g > 148 * 16) g = 148 * 16;
@@ -501,6 +556,26 @@ void sym_epilogue(Context* c, const double* rowp, const double* colp, int nb, in
   k_sym_epilogue<<<grid_for(n * t), 256, 0, c->stream>>>(rowp, colp, nb, rb, n_pass, tb, n, t,
                                                          scale, noise, noise_v, out, done);
   LGP_LAUNCH_CHECK(c);
+}
+
+void point_stats(Context* c, const double* x, int64_t n, int d, double* ctr, double* scratch,
+                 double* stats) {
+  // stats (device, d + 2 doubles): [mean (d) | max squared radius | non-finite flag]
+  const int nblk = reduce_blocks(n, 1);
+  const long long rows = chunk_rows(n, nblk);
+  int* bad = reinterpret_cast<int*>(stats + d + 1);
+  LGP_CUDA_CHECK(cudaMemsetAsync(stats, 0, (size_t)(d + 2) * sizeof(double), c->stream));
+  if (n > 0) {
+    k_pt_colsum<<<dim3(nblk, d), 256, 0, c->stream>>>(x, n, d, rows, scratch, bad);
+    LGP_LAUNCH_CHECK(c);
+  }
+  k_pt_center<<<1, 128, 0, c->stream>>>(scratch, n > 0 ? nblk : 0, d, n, ctr, stats);
+  LGP_LAUNCH_CHECK(c);
+  if (n > 0) {
+    k_pt_radius<<<grid_for(n), 256, 0, c->stream>>>(
+        x, n, d, ctr, reinterpret_cast<unsigned long long*>(stats + d));
+    LGP_LAUNCH_CHECK(c);
+  }
 }
 
 void dot_partial(Context* c, const double* a, const double* b, int64_t n, int t, double* part,

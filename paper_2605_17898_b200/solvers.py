@@ -63,9 +63,9 @@ class KernelOperator:
     Points and the compiled kernel tree are uploaded once per operator.
     """
 
-    def __init__(self, kernel, x, noise, ctx=None):
+    def __init__(self, kernel, x, noise, ctx=None, _validated=False):
         self.kernel = kernel
-        self.x = as_matrix(x, "X")
+        self.x = x if _validated else as_matrix(x, "X")
         self.noise = float(noise)
         self.n = self.x.shape[0]
         self.ctx = ctx if ctx is not None else _lib.default_context()
@@ -76,10 +76,13 @@ class KernelOperator:
         v = as_block(v, "v")
         if v.shape[0] != self.n:
             raise DimensionMismatchError(f"v has length {v.shape[0]}, X has {self.n} rows")
+        return self._matvec(v)
+
+    def _matvec(self, v):
+        # v: validated (finite, float64, C-contiguous) with n rows
         t = 1 if v.ndim == 1 else v.shape[1]
-        out = np.empty(v.shape)
+        out = _lib.result_buffer(v.shape)
         if self.n and t:
-            # v was validated by as_block above
             _lib.check(_lib.lib().lgp_matvec(self.ctx.handle, self.prog.handle, self.points.handle,
                                              self.points.handle, self.noise, _lib.vptr(v), t,
                                              _lib.vptr(out), _lib.INPUTS_FINITE))
@@ -131,7 +134,7 @@ def matrix_free_matvec(kernel, x, noise, v, block=256):
     if block < 1:
         raise ValueError("block must be at least 1")
     slab_buffer_count(kernel)  # node-protocol check, as the reference does per call
-    return KernelOperator(kernel, x, noise).matvec(v)
+    return KernelOperator(kernel, x, noise, _validated=True)._matvec(v)
 
 
 def cg_solve(apply, b, config=None):

@@ -294,3 +294,42 @@ def test_wide_point_sets_keep_accuracy(gpu_ctx, expr, d):
                                      _lib.vptr(v), 4, _lib.vptr(out), 0))
     want = O.gram(tree, xs, x) @ v
     assert rel_l2(out, want) <= TOL
+
+
+def test_points_upload_checks_on_device(gpu_ctx):
+    """lgp_points_upload validates X on the device (the C ABI may be called
+    without the Python-side checks) and keeps the centre / reach it computes."""
+    ctx = _lib.default_context()
+    x = np.random.default_rng(3).random((5000, 6))
+    bad = x.copy()
+    bad[4321, 5] = np.nan
+    h = C.c_void_p()
+    with pytest.raises(G.NonFiniteError):
+        _lib.check(_lib.lib().lgp_points_upload(ctx.handle, _lib.dptr(bad), 5000, 6, C.byref(h)))
+    bad[4321, 5] = np.inf
+    with pytest.raises(G.NonFiniteError):
+        _lib.check(_lib.lib().lgp_points_upload(ctx.handle, _lib.dptr(bad), 5000, 6, C.byref(h)))
+    # a good upload after the failures still works, results match the oracle
+    v = np.random.default_rng(4).standard_normal(5000)
+    got = G.matrix_free_matvec(G.RBF(0.7), x, 0.2, v)
+    assert rel_l2(got, O.matvec(O.parse_tree("(rbf 0.7)"), x, 0.2, v)) <= TOL
+
+
+def test_results_in_pinned_buffers_survive(gpu_ctx):
+    """Large results come back in recycled page-locked buffers; arrays that are
+    still referenced must never be overwritten by later calls."""
+    x = np.random.default_rng(5).random((20000, 4))
+    V = np.random.default_rng(6).standard_normal((20000, 16))
+    k = G.Matern52(0.6)
+    a = G.matrix_free_matvec(k, x, 0.1, V)
+    a_copy = a.copy()
+    views = [a[:, 3]]
+    for _ in range(3):
+        b = G.matrix_free_matvec(k, x, 0.1, 2.0 * V)
+        del b
+    np.testing.assert_array_equal(a, a_copy)
+    np.testing.assert_array_equal(views[0], a_copy[:, 3])
+    del a
+    c = G.matrix_free_matvec(k, x, 0.1, V)
+    np.testing.assert_array_equal(views[0], a_copy[:, 3])
+    np.testing.assert_allclose(c, a_copy, rtol=0, atol=0)
