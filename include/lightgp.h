@@ -113,6 +113,10 @@ int lgp_memcpy_d2h(lgp_ctx* ctx, void* dst, const void* src, size_t bytes);
 /* page-locked host memory (for host<->device copies at full PCIe speed) */
 int lgp_host_alloc(size_t bytes, void** out);
 int lgp_host_free(void* ptr);
+/* *all_finite = 1 iff none of p[0..n) is NaN or +-Inf (host scan, several
+   threads for large arrays; needs no GPU). The Python layer's input checks
+   (linalg.as_matrix / as_vector, reference linalg.py:91-106) use it. */
+int lgp_all_finite(const double* p, size_t n, int* all_finite);
 /* write `bytes` to a scratch buffer (L2 flush between timed iterations) */
 int lgp_flush_l2(lgp_ctx* ctx, size_t bytes);
 

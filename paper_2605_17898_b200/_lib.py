@@ -63,6 +63,7 @@ _SIGS = {
     "lgp_memcpy_d2h": ([_P, _P, _P, C.c_size_t], C.c_int),
     "lgp_host_alloc": ([C.c_size_t, C.POINTER(_P)], C.c_int),
     "lgp_host_free": ([_P], C.c_int),
+    "lgp_all_finite": ([_P, C.c_size_t, C.POINTER(C.c_int)], C.c_int),
     "lgp_flush_l2": ([_P, C.c_size_t], C.c_int),
     "lgp_kernel_compile": ([_P, C.c_int, _I32, _D, C.c_int, C.POINTER(_P)], C.c_int),
     "lgp_kernel_free": ([_P], C.c_int),
@@ -210,6 +211,13 @@ def set_default_context(ctx):
 
 
 # ------------------------------------------------------- page-locked results
+
+def all_finite(a):
+    """True iff the float64 C-contiguous array has no NaN / Inf (threaded C scan)."""
+    ok = C.c_int(0)
+    check(lib().lgp_all_finite(C.c_void_p(a.ctypes.data), a.size, C.byref(ok)))
+    return bool(ok.value)
+
 
 class _PinnedBlock:
     """A page-locked host block exposed to NumPy; returned to the pool when the

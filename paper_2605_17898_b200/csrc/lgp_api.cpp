@@ -7,6 +7,8 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "lgp_internal.h"
 
@@ -279,6 +281,39 @@ int lgp_memcpy_d2h(lgp_ctx* ctx, void* dst, const void* src, size_t bytes) {
   ctx->activate();
   LGP_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+int lgp_all_finite(const double* p, size_t n, int* all_finite) {
+  API_BEGIN
+  require(all_finite && (n == 0 || p), LGP_E_ARG, "bad lgp_all_finite arguments");
+  // a double is finite iff its exponent field is not all ones; branch-free OR
+  // (u & m) + 2^52 carries into bit 63 exactly when the exponent is all ones;
+  // adds and ORs vectorise with baseline SSE2
+  auto scan = [p](size_t lo, size_t hi) {
+    const uint64_t* u = reinterpret_cast<const uint64_t*>(p);
+    const uint64_t m = 0x7ff0000000000000ull;
+    uint64_t acc = 0;
+    for (size_t i = lo; i < hi; ++i) acc |= (u[i] & m) + (uint64_t(1) << 52);
+    return (acc >> 63) != 0;
+  };
+  const size_t kPerThread = size_t(1) << 18;  // 2 MB per thread and more
+  unsigned nt = std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency()));
+  nt = (unsigned)std::min<size_t>(nt, (n + kPerThread - 1) / kPerThread);
+  bool bad = false;
+  if (nt <= 1) {
+    bad = scan(0, n);
+  } else {
+    std::vector<char> flags(nt, 0);
+    std::vector<std::thread> th;
+    const size_t step = (n + nt - 1) / nt;
+    for (unsigned k = 1; k < nt; ++k)
+      th.emplace_back([&, k] { flags[k] = scan(std::min(n, k * step), std::min(n, (k + 1) * step)); });
+    flags[0] = scan(0, std::min(n, step));
+    for (auto& x : th) x.join();
+    for (char f : flags) bad |= f != 0;
+  }
+  *all_finite = bad ? 0 : 1;
   API_END
 }
 

@@ -51,7 +51,12 @@ def tracked(arr):
 
 
 def _finite(a, name):
-    if not np.isfinite(a).all():
+    if a.size >= (1 << 18) and a.dtype == np.float64 and a.flags.c_contiguous:
+        from . import _lib  # threaded scan in the C library (no GPU needed)
+        ok = _lib.all_finite(a)
+    else:
+        ok = bool(np.isfinite(a).all())
+    if not ok:
         raise NonFiniteError(f"{name} contains NaN or infinite entries")
 
 

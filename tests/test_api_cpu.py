@@ -168,3 +168,23 @@ def test_probe_block_matches_reference_recipe_and_prefix_stable():
     np.testing.assert_array_equal(z16, O.probes(100, 16, 3))
     np.testing.assert_array_equal(G.probe_block(100, 8, 3), z16[:, :8])
     assert set(np.unique(z16)) == {-1.0, 1.0}
+
+
+def test_threaded_finite_scan_matches_numpy():
+    """linalg's input check uses the library's threaded scan for large arrays
+    (no GPU needed); it must agree with np.isfinite on NaN / +-Inf / huge."""
+    from paper_2605_17898_b200 import _lib
+    a = np.random.default_rng(0).standard_normal(3_000_001)
+    assert _lib.all_finite(a)
+    for pos in (0, 1_499_999, 3_000_000):
+        for bad in (np.nan, np.inf, -np.inf):
+            b = a.copy()
+            b[pos] = bad
+            assert not _lib.all_finite(b)
+            with pytest.raises(G.NonFiniteError):
+                G.linalg.as_vector(b)
+    b = a.copy()
+    b[7] = np.finfo(np.float64).max
+    b[8] = -np.finfo(np.float64).tiny / 2  # subnormal
+    assert _lib.all_finite(b)
+    assert _lib.all_finite(np.empty(0))
