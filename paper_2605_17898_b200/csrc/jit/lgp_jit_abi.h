@@ -13,6 +13,7 @@ struct LgpPrepArgs {
   const double* ctr;    // d centring offsets (column mean of the column set)
   float* fr;            // [n_pad][FR] row-side features (may be null)
   float* fc;            // [n_pad][FC] column-side features (may be null)
+  float* f32;           // tensor-core prep: [n_pad][FW] FP32 features (may be null)
   long long row0;       // first point to prepare (sharded row slice)
   long long n;          // points in this slice
   long long n_pad;      // padded slice length (zero features beyond n)
@@ -54,11 +55,13 @@ struct LgpGramArgs {
 
 #ifndef LGP_TC_ABI_
 #define LGP_TC_ABI_
-// Tensor-core K1 (tcgen05, kind::tf32, 3xTF32): operands are pre-tiled in the
-// UMMA K-major no-swizzle canonical layout by the prep / pack kernels.
+// Tensor-core K1 (tcgen05, kind::f16): operands are pre-tiled in the UMMA
+// K-major no-swizzle canonical layout by the prep / pack kernels.
 struct LgpTcArgs {
-  const float* a1;      // row operand tiles   [n_rb][2 (hi,lo)][128 x KD]
-  const float* b1;      // column operand tiles [n_tiles][2][64 x KD]
+  const float* a1;      // row operand tiles (FP16 hi/lo features) [n_rb][128 x KD]
+  const float* b1;      // column operand tiles [n_tiles][64 x KD]
+  const float* r32;     // FP32 row features [n_rows_pad][FW] = (c_i, -|c_i|^2, 0..)
+  const float* c32;     // FP32 column features [n_cols_pad][FW] = (2 c_j, -|c_j|^2, 0..)
   const void* v;        // RHS tiles (FP16 hi/lo) [n_pass][n_tiles][2][TBN x 64]
   const float* vscale;  // power-of-two scale of each RHS column [n_pass * TBN]
   double* partial;      // [n_seg][n_pass][n_rows_pad][TBN]

@@ -88,7 +88,22 @@
 #define TC_VH_BYTES TC_V_BYTES
 #endif
 #define TC_NEPI (4 * (1 + LGP_TC_PAIR))  // epilogue warps arriving on PFULL / D2EMPTY
-#define TC_STAGE_BYTES (TC_B1H_BYTES + TC_VH_BYTES)
+// chunks c with bit (c % 8) set compute -r^2 on the FMA pipe from FP32
+// features instead of the distance GEMM: they need no tcgen05.ld, the K1-TC
+// roofline resource, at the cost of D + 1 FMAs and D/4 + 1 broadcast loads per
+// entry. Opt-in (LGP_TC_SIMT_MASK): measured slower on cfg4 (1 of 8 chunks:
+// 4.44 ms, 2 of 8: 4.96 ms vs 3.69 ms) - with two epilogue warps per SM
+// sub-partition the FMA chain cannot hide its latency.
+#ifndef LGP_TC_SIMT_MASK
+#define LGP_TC_SIMT_MASK 0
+#endif
+// FP32 column features of a chunk (staged only for FMA-pipe distance chunks)
+#define TC_C32_BYTES (LGP_TC_SIMT_MASK ? TC_CH * LGP_TC_FW * 4 : 0)
+#define TC_STAGE_BYTES (TC_B1H_BYTES + TC_VH_BYTES + TC_C32_BYTES)
+#if LGP_TC_PAIR && LGP_TC_SIMT_MASK
+#error "FMA-pipe distance chunks are single-CTA only"
+#endif
+#define TC_SIMT(c) ((LGP_TC_SIMT_MASK >> ((c) & 7)) & 1)
 #define TC_COMB_BYTES (128 * LGP_TC_N * 8)
 #ifndef LGP_TC_NSB
 #define LGP_TC_NSB 6   // S buffers in TMEM (64 columns each), even: NSB/2 per warpgroup
@@ -447,6 +462,19 @@ extern "C" __global__ void lgp_tc_prep(LgpPrepArgs p, int tile_rows, int is_col)
     h[3 * LGP_D + 1] = is_col ? (unsigned short)(one | sign) : nl;
     h[3 * LGP_D + 2] = is_col ? (unsigned short)(nh ^ sign) : one;
     h[3 * LGP_D + 3] = is_col ? (unsigned short)(nl ^ sign) : one;
+    // FP32 features for the chunks whose distances run on the FMA pipe:
+    // -r^2 = (-|c_i|^2) + (-|c_j|^2) + sum_d c_i[d] (2 c_j[d])
+    if (p.f32 != nullptr) {
+      float* f = p.f32 + i * LGP_TC_FW;
+#pragma unroll
+      for (int d = 0; d < LGP_D; ++d) f[d] = (float)(is_col ? 2.0 * c[d] : c[d]);
+      f[LGP_D] = (float)(-nn);
+#pragma unroll
+      for (int k = LGP_D + 1; k < LGP_TC_FW; ++k) f[k] = 0.f;
+    }
+  } else if (p.f32 != nullptr) {
+#pragma unroll
+    for (int k = 0; k < LGP_TC_FW; ++k) p.f32[i * LGP_TC_FW + k] = 0.f;
   }
   unsigned short* base = reinterpret_cast<unsigned short*>(is_col ? p.fc : p.fr) +
                          (i / tile_rows) * (long long)tile_rows * LGP_TC_KD;
@@ -566,7 +594,8 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
         if (c >= LGP_TC_STAGES) lgp_mbar_wait(BAR(B_SEMPTY(s)), ((c / LGP_TC_STAGES) - 1) & 1);
         TR_MARK(0)
         const unsigned dst = lgp_saddr(stg + (size_t)s * TC_STAGE_BYTES);
-        lgp_mbar_expect_tx(BAR(B_SFULL(s)), TC_STAGE_BYTES);
+        lgp_mbar_expect_tx(BAR(B_SFULL(s)),
+                           TC_B1H_BYTES + TC_VH_BYTES + (TC_SIMT(c) ? TC_C32_BYTES : 0));
         lgp_bulk_g2s(dst,
                      reinterpret_cast<const unsigned char*>(a.b1) +
                          (size_t)(tile0 + c) * TC_B1_BYTES + rank * TC_B1H_BYTES,
@@ -575,6 +604,11 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
                      vbase + ((size_t)pass * a.n_tiles + tile0 + c) * TC_V_BYTES +
                          rank * TC_VH_BYTES,
                      TC_VH_BYTES, BAR(B_SFULL(s)));
+        if (TC_SIMT(c))
+          lgp_bulk_g2s(dst + TC_B1H_BYTES + TC_VH_BYTES,
+                       reinterpret_cast<const unsigned char*>(a.c32) +
+                           (size_t)(tile0 + c) * TC_C32_BYTES,
+                       TC_C32_BYTES, BAR(B_SFULL(s)));
         TR_MARK(1)
       }
       TR_FLUSH(0, 1)
@@ -592,6 +626,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
 #endif
       TR_DECL
       for (int c = 0; c < nch; ++c) {
+        if (TC_SIMT(c)) continue;  // distances of this chunk come from the FMA pipe
         const int w = c & 1, k = c >> 1;
         const int q = w + 2 * (k % TC_NSBW);
         const int s = c % LGP_TC_STAGES;
@@ -680,6 +715,11 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
     double acc[LGP_TC_N];
 #pragma unroll
     for (int i = 0; i < LGP_TC_N; ++i) acc[i] = 0.0;
+#if LGP_TC_SIMT_MASK
+    float rf32[LGP_D + 1];  // this thread's row: (c_i, -|c_i|^2)
+#pragma unroll
+    for (int d = 0; d <= LGP_D; ++d) rf32[d] = a.r32[((size_t)rb * 128 + row) * LGP_TC_FW + d];
+#endif
 
     auto drain = [&](int gi) {
       const int b = gi & 1;
@@ -700,19 +740,57 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
     };
 
     TR_DECL
+    // S1FULL(q) completes once per distance-GEMM use of buffer q; with
+    // FMA-pipe chunks interleaved, its phase is tracked per buffer slot
+    unsigned s1par = 0;
     for (int k = 0; k < nloc; ++k) {
       const int q = w + 2 * (k % TC_NSBW);
       const unsigned sb = T_SB(q) + lanes;
-      if (lane == 0) { TR_MARK(8) }
-      lgp_mbar_wait(BAR(B_S1FULL(q)), (k / TC_NSBW) & 1);
-      if (lane == 0) { TR_MARK(9) }
-      lgp_tc_fence_after();
-      // all 64 columns in one round trip; P overwrites S' in the same
-      // registers: s[2m] = FP16x2 hi of entries (2m, 2m+1), s[2m+1] = lo
       unsigned s[64];
-      lgp_tmem_ld32p(sb, s);
-      lgp_tmem_ld32p(sb + 32u, s + 32);
-      lgp_tmem_wait_ld();
+      if (lane == 0) { TR_MARK(8) }
+#if LGP_TC_SIMT_MASK
+      const int c = 2 * k + w;
+      if (TC_SIMT(c)) {
+        // -r^2 on the FMA pipe from the staged FP32 column features (every
+        // lane reads the same column: broadcast); the S buffer is free once
+        // the contraction that last read it has completed
+        const int st = c % LGP_TC_STAGES;
+        lgp_mbar_wait(BAR(B_SFULL(st)), (c / LGP_TC_STAGES) & 1);
+        if (k >= TC_NSBW) lgp_mbar_wait(BAR(B_PEMPTY(q)), ((k / TC_NSBW) - 1) & 1);
+        if (lane == 0) { TR_MARK(9) }
+        lgp_tc_fence_after();
+        const float4* cf = reinterpret_cast<const float4*>(
+            stg + (size_t)st * TC_STAGE_BYTES + TC_B1H_BYTES + TC_VH_BYTES);
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          float cj[LGP_TC_FW];
+#pragma unroll
+          for (int f4 = 0; f4 < LGP_TC_FW / 4; ++f4) {
+            const float4 v4 = cf[j * (LGP_TC_FW / 4) + f4];
+            cj[4 * f4 + 0] = v4.x;
+            cj[4 * f4 + 1] = v4.y;
+            cj[4 * f4 + 2] = v4.z;
+            cj[4 * f4 + 3] = v4.w;
+          }
+          float acc = rf32[LGP_D] + cj[LGP_D];
+#pragma unroll
+          for (int d = 0; d < LGP_D; ++d) acc = fmaf(rf32[d], cj[d], acc);
+          s[j] = __float_as_uint(acc);
+        }
+      } else
+#endif
+      {
+        const int slot = k % TC_NSBW;
+        lgp_mbar_wait(BAR(B_S1FULL(q)), (s1par >> slot) & 1u);
+        s1par ^= 1u << slot;
+        if (lane == 0) { TR_MARK(9) }
+        lgp_tc_fence_after();
+        // all 64 columns in one round trip; P overwrites S' in the same
+        // registers: s[2m] = FP16x2 hi of entries (2m, 2m+1), s[2m+1] = lo
+        lgp_tmem_ld32p(sb, s);
+        lgp_tmem_ld32p(sb + 32u, s + 32);
+        lgp_tmem_wait_ld();
+      }
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
         const int px = (m & 7) < (LGP_TC_POLY + 1) / 2 ? 1 : 0;

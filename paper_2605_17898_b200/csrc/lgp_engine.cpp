@@ -135,6 +135,10 @@ void MatvecOp::prepare() {
     // operands pre-tiled in the UMMA canonical layout, FP16 hi/lo split
     fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * plan.tc_kd * 2);
     fc = (float*)ctx->scratch_get(tag + ".b1", (size_t)n_cols_pad * plan.tc_kd * 2);
+    if (plan.tc_simt) {
+      r32 = (float*)ctx->scratch_get(tag + ".r32", (size_t)n_rows_pad * plan.tc_fw * 4);
+      c32 = (float*)ctx->scratch_get(tag + ".c32", (size_t)n_cols_pad * plan.tc_fw * 4);
+    }
     vtc = ctx->scratch_get(tag + ".vtc", (size_t)n_pass * n_cols_pad * 2 * tb * 2);
     vscale = (float*)ctx->scratch_get(tag + ".vscale", (size_t)n_pass * tb * 4);
     v_inexact = (int*)ctx->scratch_get(tag + ".vflag", 16);
@@ -143,6 +147,7 @@ void MatvecOp::prepare() {
     pa.ctr = cols->ctr;
     pa.fr = fr;
     pa.fc = fc;
+    pa.f32 = r32;
     pa.row0 = row0;
     pa.n = n_rows;
     pa.n_pad = n_rows_pad;
@@ -156,6 +161,7 @@ void MatvecOp::prepare() {
     pc.ctr = cols->ctr;
     pc.fr = fr;
     pc.fc = fc;
+    pc.f32 = c32;
     pc.row0 = 0;
     pc.n = cols->n;
     pc.n_pad = n_cols_pad;
@@ -241,6 +247,8 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     a.vscale = vscale;
     a.a1 = fr;
     a.b1 = fc;
+    a.r32 = r32;
+    a.c32 = c32;
     a.v = vtc;
     a.partial = partial;
     a.done = done;

@@ -100,6 +100,8 @@ struct Plan {
   int tc_kd = 0;            // K of the distance GEMM in FP16 halves (3D + 4, multiple of 16)
   int tc_n = 16;            // RHS per pass (GEMM2 N)
   bool tc_pair = false;     // K1-TC on CTA pairs (cta_group::2, 256-row blocks)
+  int tc_fw = 0;            // FP32 features per point for FMA-pipe distance chunks
+  bool tc_simt = false;     // some K1-TC chunks compute distances on the FMA pipe
   LgpTcArgs tca{};          // kc[] filled
 };
 
@@ -214,6 +216,8 @@ struct MatvecOp {
   int* units = nullptr;
   double* colpart = nullptr;
   size_t smem_sym = 0;
+  float* r32 = nullptr;     // K1-TC FP32 row / column features
+  float* c32 = nullptr;
   float* fr = nullptr;
   float* fc = nullptr;
   double* vpack = nullptr;

@@ -333,3 +333,18 @@ def test_results_in_pinned_buffers_survive(gpu_ctx):
     c = G.matrix_free_matvec(k, x, 0.1, V)
     np.testing.assert_array_equal(views[0], a_copy[:, 3])
     np.testing.assert_allclose(c, a_copy, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("env", [{"LGP_TC_PAIR": "1"}, {"LGP_TC_SIMT_MASK": "0x48"},
+                                 {"LGP_TC_POLY": "0"}, {"LGP_TC_G": "2", "LGP_TC_DLAG": "1"}])
+def test_tensor_core_variants_parity(gpu_ctx, monkeypatch, env):
+    """The opt-in K1-TC variants (CTA pairs with cta_group::2, FMA-pipe distance
+    chunks, MUFU-only exp2, other drain schedules) meet the same bar."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    expr = "(+ (scale 2.0 (rbf 0.4)) (scale 0.5 (matern32 0.9)))"
+    rng = np.random.default_rng(11)
+    x = rng.random((3001, 6))
+    V = rng.standard_normal((3001, 16))
+    got = _mv_flags(expr, x, V, 0.1, 0)
+    assert rel_l2(got, O.matvec(O.parse_tree(expr), x, 0.1, V)) <= TOL
