@@ -1,0 +1,104 @@
+"""Full-size ("tier C") golden values from the REAL reference.
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_tierc.py cfg2
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_tierc.py cfg4
+
+Build container only (the reference is not on the GPU box).
+
+fullsize_cfg2.npz  cfg2 in full (N = 20000, Matern-5/2, D = 4): the reference's own
+                   cg_solve / slq_logdet / mean / LML code on the "dense replay"
+                   operator (kernel_eval(X, X) + noise I, applied with dgemv: the
+                   same kernel entries as matrix_free_matvec, only the summation
+                   order of the matvec differs), plus the exact
+                   (Cholesky) latent variance at 200 test points.
+tierc_cfg4.npz     cfg4 in full (N = 100000, RBF, D = 8) through the reference's
+                   real matrix_free_matvec (block = 32, the fit's block): CG after
+                   exactly 20 iterations, and the SLQ quadratures of 16 probes
+                   after 5 Lanczos steps (equal, pinned budgets; ~1.5 h of CPU).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+import scipy.linalg
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "..", ".."))
+
+import minigp as M  # noqa: E402  (reference, build container only)
+import minigp.solvers as MS  # noqa: E402
+
+from oracle import gp_oracle as O  # noqa: E402  (shared input recipe only)
+
+
+def log(*a):
+    print(time.strftime("%H:%M:%S"), *a, flush=True)
+
+
+def cfg2():
+    cfg = O.CONFIGS["cfg2"]
+    x, y = O.synthetic(cfg["n"], cfg["d"])
+    n = x.shape[0]
+    k = M.parse_kernel(cfg["kernel"])
+    noise = cfg["noise"]
+    log("cfg2 gram")
+    gram_y = M.kernel_eval(k, x)
+    gram_y.flat[:: n + 1] += noise
+    apply = lambda v: gram_y @ v  # noqa: E731
+    fit_cfg = M.CgConfig(rel_tolerance=1e-8)  # models.py FIT_CG_TOLERANCE
+    log("cfg2 CG")
+    res = M.cg_solve(apply, y, fit_cfg)
+    log("cfg2 CG", res.iterations, res.final_residual)
+    ld = M.slq_logdet(apply, n, fit_cfg, seed=0)
+    quad = float(y @ res.x)
+    lml = -0.5 * (quad + ld + n * np.log(2 * np.pi))
+    log("cfg2 SLQ logdet", ld, "LML", lml)
+    xs = np.random.default_rng(9).random((200, cfg["d"]))
+    kstar = M.kernel_eval(k, x, xs)
+    mean = kstar.T @ res.x
+    log("cfg2 Cholesky")
+    c = scipy.linalg.cho_factor(gram_y, lower=True, overwrite_a=False, check_finite=False)
+    half = scipy.linalg.solve_triangular(c[0], kstar, lower=True, check_finite=False)
+    var = np.maximum(M.kernel_diag(k, xs) - np.einsum("ij,ij->j", half, half), 0.0)
+    chol_alpha = scipy.linalg.cho_solve(c, y, check_finite=False)
+    np.savez_compressed(
+        os.path.join(HERE, "fullsize_cfg2.npz"), it=res.iterations, res=res.final_residual,
+        alpha=res.x, logdet=ld, lml=lml, mean=mean, var=var, chol_mean=kstar.T @ chol_alpha,
+        note="reference cg_solve/slq_logdet on the dense replay operator; var by Cholesky")
+    log("cfg2 done")
+
+
+def cfg4():
+    cfg = O.CONFIGS["cfg4"]
+    x, y = O.synthetic(cfg["n"], cfg["d"])
+    n = x.shape[0]
+    k = M.parse_kernel(cfg["kernel"])
+    noise = cfg["noise"]
+    apply = lambda v: M.matrix_free_matvec(k, x, noise, v, block=32)  # noqa: E731
+    it = 20
+    log("cfg4 CG", it, "iterations")
+    res = M.cg_solve(apply, y, M.CgConfig(rel_tolerance=1e-30, max_iterations=it))
+    log("cfg4 CG", res.iterations, res.final_residual)
+    np.savez_compressed(os.path.join(HERE, "tierc_cfg4_cg.npz"), it=res.iterations,
+                        res=res.final_residual, x=res.x)
+    steps, probes = 5, 16
+    z = O.probes(n, probes, seed=0)
+    quads = np.zeros(probes)
+    for c in range(probes):
+        quads[c] = MS._lanczos_quadrature(apply, np.ascontiguousarray(z[:, c]), steps)
+        log("cfg4 probe", c, quads[c])
+    np.savez_compressed(
+        os.path.join(HERE, "tierc_cfg4.npz"), it=res.iterations, res=res.final_residual,
+        x=res.x, steps=steps, probes=probes, quads=quads,
+        note="reference matrix_free_matvec (block 32): CG after 20 iterations, "
+             "per-probe Lanczos quadratures after 5 steps (probe seed 0)")
+    log("cfg4 done")
+
+
+if __name__ == "__main__":
+    for name in sys.argv[1:]:
+        {"cfg2": cfg2, "cfg4": cfg4}[name]()
