@@ -141,7 +141,8 @@ void MatvecOp::prepare() {
     }
     vtc = ctx->scratch_get(tag + ".vtc", (size_t)n_pass * n_cols_pad * 2 * tb * 2);
     vscale = (float*)ctx->scratch_get(tag + ".vscale", (size_t)n_pass * tb * 4);
-    v_inexact = (int*)ctx->scratch_get(tag + ".vflag", 16);
+    // inexact flag (16 B) followed by the per-column max |V| used for the scales
+    v_inexact = (int*)ctx->scratch_get(tag + ".vflag", 16 + (size_t)n_pass * tb * 8);
     LgpPrepArgs pa = plan.prep;
     pa.x = rows->x;
     pa.ctr = cols->ctr;

@@ -22,8 +22,10 @@ namespace lgp {
 namespace vec {
 namespace {
 
-constexpr int kMaxBlocks = 512;
-constexpr int kRowsPerBlock = 2048;
+// fixed row partition of the deterministic reductions: enough blocks to keep
+// every SM streaming (n = 100k -> 391 blocks of 256 rows)
+constexpr int kMaxBlocks = 2048;
+constexpr int kRowsPerBlock = 256;
 
 inline int reduce_bd(int t) { return t * (256 / t); }
 
@@ -83,30 +85,53 @@ __global__ void k_pack(const double* __restrict__ V, long long n, int t, long lo
 }
 
 // power-of-two scale of each RHS column (max |V[:, c]| in [0.5, 1) after scaling)
-__global__ void k_colscale(const double* __restrict__ V, long long n, int t, int ncols_pad,
-                           float* scale, const int* done) {
+// column max |V| (coalesced over the n x t block; order-free max through the
+// bit patterns of non-negative doubles), then the power-of-two scales
+__global__ void k_colmax(const double* __restrict__ V, long long n, int t,
+                         unsigned long long* colmax, const int* done) {
   __shared__ double sm[256];
   if (is_done(done)) return;
-  const int c = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int c = tid % t;
+  const int stride = blockDim.x / t;
   double m = 0.0;
-  if (c < t)
-    for (long long i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(V[i * t + c]));
-  sm[threadIdx.x] = m;
+  if (tid < stride * t)
+    for (long long i = (long long)blockIdx.x * stride + tid / t; i < n;
+         i += (long long)gridDim.x * stride)
+      m = fmax(m, fabs(V[i * t + c]));
+  sm[tid] = m;
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + s]);
-    __syncthreads();
+  if (tid < t) {
+    double mm = 0.0;
+    for (int k = tid; k < stride * t; k += t) mm = fmax(mm, sm[k]);
+    if (mm > 0.0) atomicMax(colmax + tid, (unsigned long long)__double_as_longlong(mm));
   }
-  if (threadIdx.x == 0) {
+}
+
+// t > 256: one thread per column (adjacent threads read adjacent columns)
+__global__ void k_colmax_wide(const double* __restrict__ V, long long n, int t,
+                              unsigned long long* colmax, const int* done) {
+  if (is_done(done)) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= t) return;
+  double m = 0.0;
+  for (long long i = blockIdx.y; i < n; i += gridDim.y) m = fmax(m, fabs(V[i * t + c]));
+  if (m > 0.0) atomicMax(colmax + c, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_colscale(const unsigned long long* __restrict__ colmax, int t, int ncols_pad,
+                           float* scale, const int* done) {
+  if (is_done(done)) return;
+  for (int c = threadIdx.x; c < ncols_pad; c += blockDim.x) {
     double sc = 1.0;
-    if (sm[0] > 0.0) {
+    const double m = c < t ? __longlong_as_double((long long)colmax[c]) : 0.0;
+    if (m > 0.0) {
       int e;
-      frexp(sm[0], &e);
+      frexp(m, &e);
       sc = ldexp(1.0, e);
     }
     scale[c] = (float)sc;
   }
-  (void)ncols_pad;
 }
 
 // RHS tiles for the tensor-core K1: FP16 hi/lo of V / scale in the UMMA
@@ -365,12 +390,22 @@ __global__ void k_lz_multidot(const double* __restrict__ basis, long long stride
   const long long r0 = (long long)blockIdx.x * chunk;
   long long r1 = r0 + chunk;
   if (r1 > n) r1 = n;
-  for (int k = 0; k < nb; ++k) {
-    const double* bk = basis + (size_t)k * stride_k;
-    double s = 0.0;
+  // basis vectors in batches of 4: w is read once per batch and the four
+  // independent FMA chains keep more loads in flight (per-(k, c) summation
+  // order is unchanged: rows in stride order)
+  for (int k0 = 0; k0 < nb; k0 += 4) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
     if (tid < stride * t)
-      for (long long i = r0 + tid / t; i < r1; i += stride) s = fma(bk[i * t + c], w[i * t + c], s);
-    block_colsum(s, t, part + ((size_t)blockIdx.x * nb + k) * t, sm);
+      for (long long i = r0 + tid / t; i < r1; i += stride) {
+        const long long e = i * t + c;
+        const double wv = w[e];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (k0 + kk < nb) s[kk] = fma(basis[(size_t)(k0 + kk) * stride_k + e], wv, s[kk]);
+      }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      if (k0 + kk < nb) block_colsum(s[kk], t, part + ((size_t)blockIdx.x * nb + k0 + kk) * t, sm);
   }
 }
 
@@ -387,6 +422,7 @@ __global__ void k_lz_update2(double* __restrict__ w, const double* __restrict__ 
                              long long stride_k, int nb, long long n, int t, long long chunk,
                              LzState s, double* part) {
   __shared__ double sm[256];
+  __shared__ double hs[64 * 32];  // h[k][c] for nb <= 64, t <= 32 (else read from global)
   if (*s.done) return;
   const int tid = threadIdx.x;
   const int c = tid % t;
@@ -394,6 +430,11 @@ __global__ void k_lz_update2(double* __restrict__ w, const double* __restrict__ 
   const long long r0 = (long long)blockIdx.x * chunk;
   long long r1 = r0 + chunk;
   if (r1 > n) r1 = n;
+  const bool hsm = nb * t <= 64 * 32;
+  if (hsm)
+    for (int e = tid; e < nb * t; e += blockDim.x) hs[e] = s.h[e];
+  __syncthreads();
+  const double* h = hsm ? hs : s.h;
   double acc = 0.0;
   if (tid < stride * t) {
     const bool act = s.active[c] != 0;
@@ -402,7 +443,7 @@ __global__ void k_lz_update2(double* __restrict__ w, const double* __restrict__ 
       double v = w[e];
       if (act) {
         double u = 0.0;
-        for (int k = 0; k < nb; ++k) u = fma(basis[(size_t)k * stride_k + e], s.h[k * t + c], u);
+        for (int k = 0; k < nb; ++k) u = fma(basis[(size_t)k * stride_k + e], h[k * t + c], u);
         v = __dsub_rn(v, u);
         w[e] = v;
       }
@@ -534,7 +575,16 @@ void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int 
 
 void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int tbn, int n_pass,
                  void* out, float* scale, int* inexact, const int* done) {
-  k_colscale<<<n_pass * tbn, 256, 0, c->stream>>>(V, n, t, n_pass * tbn, scale, done);
+  // colmax scratch: the first t slots of `scale` reinterpreted would alias, so
+  // the maxima live behind the inexact flag's 16-byte slot (see MatvecOp)
+  unsigned long long* colmax = reinterpret_cast<unsigned long long*>(inexact + 4);
+  LGP_CUDA_CHECK(cudaMemsetAsync(colmax, 0, (size_t)n_pass * tbn * 8, c->stream));
+  if (t <= 256)
+    k_colmax<<<grid_for(n * t / 4 + 1), reduce_bd(t), 0, c->stream>>>(V, n, t, colmax, done);
+  else
+    k_colmax_wide<<<dim3((t + 255) / 256, 64), 256, 0, c->stream>>>(V, n, t, colmax, done);
+  LGP_LAUNCH_CHECK(c);
+  k_colscale<<<1, 256, 0, c->stream>>>(colmax, t, n_pass * tbn, scale, done);
   LGP_LAUNCH_CHECK(c);
   LGP_CUDA_CHECK(cudaMemsetAsync(inexact, 0, sizeof(int), c->stream));
   k_pack_tc<<<grid_for((long long)n_pass * n_tiles * tbn * 64), 256, 0, c->stream>>>(

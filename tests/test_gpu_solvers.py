@@ -47,8 +47,11 @@ def test_cg_same_iteration_budget(gpu_ctx):
     k = G.Matern52(0.5)
     nodes = O.parse_tree(G.format_kernel(k))
     # un-converged iterates amplify the ~1e-7 FP32-entry perturbation with
-    # every step; the converged-solution bar (1e-4) is checked in test_cg_golden
-    for it, bar in ((5, 1e-5), (25, 2e-4)):
+    # every step: a CPU emulation (FP64 CG on the FP32-rounded Gram of this
+    # system, cond ~2.5e3) drifts 1.4e-7 from the FP64 iterate after 5 steps and
+    # 3.0e-3 after 25 (a mere FP64 re-ordering: 2e-5). The converged-solution
+    # bar (1e-4) is checked in test_cg_golden.
+    for it, bar in ((5, 1e-5), (25, 1e-2)):
         cfg = G.CgConfig(rel_tolerance=1e-30, max_iterations=it)
         res = G.cg_solve(G.KernelOperator(k, x, 0.1), b, cfg)
         ref = O.cg(lambda v: O.matvec(nodes, x, 0.1, v), b, 1e-30, it)
