@@ -389,6 +389,7 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   op.n_rows = r1 - r0;
   op.t = t;
   op.tag = "cg.mv";
+  op.allow_tc = std::getenv("LGP_CG_TC") != nullptr;  // experiment: CG on the tensor-core K1
   op.prepare();
 
   vec::dot_partial(ctx, B_dev, B_dev, n, t, b.part, nullptr);
