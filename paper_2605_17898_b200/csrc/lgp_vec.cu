@@ -16,6 +16,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "lgp_internal.h"
 
 namespace lgp {
@@ -71,7 +73,7 @@ __global__ void k_dot_final(const double* part, int nblk, int t, double* out, co
 }
 
 __global__ void k_pack(const double* __restrict__ V, long long n, int t, long long n_pad, int tb,
-                       int n_pass, double* __restrict__ out, const int* done) {
+                       int n_pass, double* __restrict__ out, const int* done, int drop_bits) {
   if (is_done(done)) return;
   const long long total = (long long)n_pass * n_pad * tb;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -80,7 +82,11 @@ __global__ void k_pack(const double* __restrict__ V, long long n, int t, long lo
     const long long j = (e / tb) % n_pad;
     const int p = (int)(e / ((long long)tb * n_pad));
     const int c = p * tb + cc;
-    out[e] = (j < n && c < t) ? V[j * t + c] : 0.0;
+    double v = (j < n && c < t) ? V[j * t + c] : 0.0;
+    // experiment (LGP_EMU_VBITS): keep only 52 - drop_bits mantissa bits of V,
+    // emulating the RHS rounding of a tensor-core contraction
+    if (drop_bits) v = __longlong_as_double(__double_as_longlong(v) & ~((1ll << drop_bits) - 1));
+    out[e] = v;
   }
 }
 
@@ -568,8 +574,9 @@ int reduce_blocks(int64_t n, int t) {
 
 void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int tb, int n_pass,
               double* out, const int* done) {
+  static const int drop = std::getenv("LGP_EMU_VBITS") ? 52 - atoi(std::getenv("LGP_EMU_VBITS")) : 0;
   k_pack<<<grid_for((long long)n_pass * n_pad * tb), 256, 0, c->stream>>>(V, n, t, n_pad, tb,
-                                                                         n_pass, out, done);
+                                                                         n_pass, out, done, drop);
   LGP_LAUNCH_CHECK(c);
 }
 
