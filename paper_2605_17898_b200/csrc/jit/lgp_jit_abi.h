@@ -77,4 +77,20 @@ struct LgpTcArgs {
   int pad_[2];
   float kc[LGP_MAX_KC];
 };
+
+// Symmetric tensor-core K1 for the square operator with one RHS (the CG
+// matvec): every unordered pair (i, j) is evaluated once, in the tile of row
+// block min and column chunk max, and feeds out_i and out_j in FP64.
+struct LgpTcSymArgs {
+  const float* a1;            // row operand tiles (FP16 hi/lo features) [n_rb][128 x KD]
+  const float* b1;            // column operand tiles [n_tiles][64 x KD]
+  const double* v;            // RHS, zero-padded to the column padding (t = 1)
+  const int* items;           // [n_items][3]: row block I, chunk range [c0, c1)
+  const long long* colbase;   // [n_rb]: first column-partial record of row block I
+  double* rowpart;            // [n_items][128]
+  double* colpart;            // [records][64]: record (I, c) at colbase[I] + c - 2I
+  const int* done;            // optional early-exit flag
+  unsigned long long* trace;  // LGP_TC_TRACE builds only
+  float kc[LGP_MAX_KC];
+};
 #endif

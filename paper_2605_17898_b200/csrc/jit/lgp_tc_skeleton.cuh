@@ -128,6 +128,14 @@
 #define B_D2EMPTY(w, b) (6 + 3 * LGP_TC_STAGES + 2 * LGP_TC_NSB + 2 * (w) + (b))
 #define B_PEMPTY(q) (10 + 3 * LGP_TC_STAGES + 2 * LGP_TC_NSB + (q))
 
+// blocking mbarrier waits let the hardware suspend the waiting thread (up to
+// this many ns per try) instead of spinning: spinning producer / issuer /
+// epilogue warps steal issue slots from the working warps of their SM
+// sub-partition
+#ifndef LGP_TC_SUSPEND_NS
+#define LGP_TC_SUSPEND_NS 20000
+#endif
+
 __device__ __forceinline__ float lgp_ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -206,10 +214,10 @@ __device__ __forceinline__ void lgp_mbar_wait(unsigned bar, unsigned parity) {
 #endif
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "r"(LGP_TC_SUSPEND_NS)
         : "memory");
   }
 }
@@ -256,10 +264,10 @@ __device__ __forceinline__ void lgp_mbar_wait_cl(unsigned bar, unsigned parity) 
 #endif
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "r"(LGP_TC_SUSPEND_NS)
         : "memory");
   }
 }

@@ -1,0 +1,225 @@
+// JIT skeleton of the symmetric tensor-core matvec (K1-TC-sym) for the square
+// operator with one right-hand side: the CG matvec (K(X,X) + noise I) p.
+// Appended after lgp_tc_skeleton.cuh (shares its helpers, the feature tiles
+// and the generated lgp_tc_k()).
+//
+// Exact symmetry is what CG needs (profiles/r01_cg_tc_experiment.txt: a
+// rounding-level asymmetric operator or a rounded direction vector costs 8-50 %
+// more iterations), so:
+//   * each unordered pair {i, j} is evaluated ONCE, in the tile of row block
+//     I = block(min) and column chunk c = chunk(max), by the distance GEMM
+//     (tcgen05 kind::f16, -r^2 in TMEM) and the tree on one epilogue thread,
+//     and that single FP32 value k_ij feeds both out_i and out_j;
+//   * the contraction stays FP64 with the exact FP64 p: the row side is one
+//     DFMA per entry in the row's thread, the column side k_ij * p_i is reduced
+//     over the warp's 32 rows by a transpose-reduce butterfly (after 5 levels
+//     lane l holds column l) and over the 4 warps in a fixed order.
+// Diagonal tiles: entries j > i go to both sides, j == i to the row side only,
+// j < i are skipped (they are the pair's other orientation). Partials (row:
+// per (I, segment); column: per (I, chunk)) are summed in a fixed order by
+// k_tcsym_epilogue (deterministic).
+//
+// CTA = one row block I (128 rows, one TMEM lane each) x a segment of its
+// column chunks [c0, c1) (c0 >= 2I). Warps: 0 producer (cp.async.bulk ring of
+// column-feature tiles + p chunks), 1 distance-GEMM issuer, 2..9 two epilogue
+// warpgroups taking even / odd chunks.
+
+#define TS_THREADS 320
+#define TS_VCH_BYTES (TC_CH * 8)                        // p chunk, FP64
+#define TS_STAGE_BYTES (TC_B1_BYTES + TS_VCH_BYTES)
+#define TS_CBUF_BYTES (2 * 2 * 4 * TC_CH * 8)           // [wg][parity][warp][64] FP64
+#define TS_NBARS (1 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB)
+#define TSB_AFULL 0
+#define TSB_SFULL(s) (1 + (s))
+#define TSB_SEMPTY(s) (1 + LGP_TC_STAGES + (s))
+#define TSB_S1FULL(q) (1 + 2 * LGP_TC_STAGES + (q))
+#define TSB_SFREE(q) (1 + 2 * LGP_TC_STAGES + LGP_TC_NSB + (q))
+
+// FP32 -> FP64 for finite non-negative kernel values without the conversion
+// pipe: exponent re-bias + mantissa shift (0 maps to 2^-127, negligible)
+__device__ __forceinline__ double lgp_widen_nn(float f) {
+  const unsigned b = __float_as_uint(f);
+  return __hiloint2double((b >> 3) + 0x38000000u, b << 29);
+}
+
+extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(const LgpTcSymArgs a) {
+  if (a.done != nullptr && *a.done) return;
+  const int item = blockIdx.x;
+  const int I = a.items[3 * item], c0 = a.items[3 * item + 1], c1 = a.items[3 * item + 2];
+  const int nch = c1 - c0;
+
+  extern __shared__ __align__(1024) unsigned char ts_smem[];
+  unsigned char* a1s = ts_smem;
+  double* vis = reinterpret_cast<double*>(ts_smem + TC_A1_BYTES);  // p of the 128 rows
+  unsigned char* stg = ts_smem + TC_A1_BYTES + 128 * 8;
+  double* cbuf = reinterpret_cast<double*>(stg + LGP_TC_STAGES * TS_STAGE_BYTES);
+  double* comb = cbuf + TS_CBUF_BYTES / 8;  // [128] warpgroup 1's row sums
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(comb + 128);
+  unsigned* tslot = reinterpret_cast<unsigned*>(bars + TS_NBARS);
+  const unsigned bar0 = lgp_saddr(bars);
+#define TBAR(i) (bar0 + 8u * (unsigned)(i))
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+
+  if (tid == 0) {
+    lgp_mbar_init(TBAR(TSB_AFULL), 1);
+    for (int s = 0; s < LGP_TC_STAGES; ++s) {
+      lgp_mbar_init(TBAR(TSB_SFULL(s)), 1);
+      lgp_mbar_init(TBAR(TSB_SEMPTY(s)), 4);  // the 4 warps of the chunk's warpgroup
+    }
+    for (int q = 0; q < LGP_TC_NSB; ++q) {
+      lgp_mbar_init(TBAR(TSB_S1FULL(q)), 1);
+      lgp_mbar_init(TBAR(TSB_SFREE(q)), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     lgp_saddr(tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  lgp_tc_fence_before();
+  __syncthreads();
+  lgp_tc_fence_after();
+  const unsigned tmem = *tslot;
+#define TS_SB(q) (tmem + 64u * (unsigned)(q))
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ producer (TMA bulk)
+      lgp_mbar_expect_tx(TBAR(TSB_AFULL), TC_A1_BYTES + 128 * 8);
+      lgp_bulk_g2s(lgp_saddr(a1s), a.a1 + (size_t)I * (TC_A1_BYTES / 4), TC_A1_BYTES,
+                   TBAR(TSB_AFULL));
+      lgp_bulk_g2s(lgp_saddr(vis), a.v + (size_t)I * 128, 128 * 8, TBAR(TSB_AFULL));
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % LGP_TC_STAGES;
+        if (c >= LGP_TC_STAGES) lgp_mbar_wait(TBAR(TSB_SEMPTY(s)), ((c / LGP_TC_STAGES) - 1) & 1);
+        const unsigned dst = lgp_saddr(stg + (size_t)s * TS_STAGE_BYTES);
+        lgp_mbar_expect_tx(TBAR(TSB_SFULL(s)), TS_STAGE_BYTES);
+        lgp_bulk_g2s(dst,
+                     reinterpret_cast<const unsigned char*>(a.b1) + (size_t)(c0 + c) * TC_B1_BYTES,
+                     TC_B1_BYTES, TBAR(TSB_SFULL(s)));
+        lgp_bulk_g2s(dst + TC_B1_BYTES, a.v + (size_t)(c0 + c) * TC_CH, TS_VCH_BYTES,
+                     TBAR(TSB_SFULL(s)));
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------- distance-GEMM issuer
+      const unsigned idesc1 = (1u << 4) | ((unsigned)(TC_CH >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
+      const unsigned long long dk = lgp_sdesc(0u, LGP_TC_KD * 16);
+      const unsigned long long a_d = dk + (lgp_saddr(a1s) >> 4);
+      const unsigned stg0 = lgp_saddr(stg) >> 4;
+      lgp_mbar_wait(TBAR(TSB_AFULL), 0);
+      for (int c = 0; c < nch; ++c) {
+        const int w = c & 1, k = c >> 1;
+        const int q = w + 2 * (k % TC_NSBW);
+        const int s = c % LGP_TC_STAGES;
+        lgp_mbar_wait(TBAR(TSB_SFULL(s)), (c / LGP_TC_STAGES) & 1);
+        if (k >= TC_NSBW) lgp_mbar_wait(TBAR(TSB_SFREE(q)), ((k / TC_NSBW) - 1) & 1);
+        lgp_tc_fence_after();
+        const unsigned long long b_d = dk + stg0 + (unsigned)s * (TS_STAGE_BYTES >> 4);
+#pragma unroll
+        for (int kk = 0; kk < LGP_TC_KD / 16; ++kk)
+          lgp_mma_f16_ss(TS_SB(q), a_d + 16u * kk, b_d + 16u * kk, idesc1, kk > 0);
+        lgp_mma_commit(TBAR(TSB_S1FULL(q)));
+      }
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------------------- epilogue warpgroups
+    const int w = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int row = 32 * q4 + lane;
+    const unsigned lanes = (unsigned)(32 * q4) << 16;
+    const int nloc = (nch - w + 1) >> 1;
+    const long long gi = 128ll * I + row;
+    lgp_mbar_wait(TBAR(TSB_AFULL), 0);
+    const double vi = vis[row];
+    double acc = 0.0;
+    for (int k = 0; k < nloc; ++k) {
+      const int c = 2 * k + w;
+      const int q = w + 2 * (k % TC_NSBW);
+      const int s = c % LGP_TC_STAGES;
+      const int chunk = c0 + c;
+      lgp_mbar_wait(TBAR(TSB_S1FULL(q)), (k / TC_NSBW) & 1);
+      lgp_tc_fence_after();
+      unsigned sv[64];
+      lgp_tmem_ld32p(TS_SB(q) + lanes, sv);
+      lgp_tmem_ld32p(TS_SB(q) + lanes + 32u, sv + 32);
+      lgp_tmem_wait_ld();
+      lgp_tc_fence_before();
+      __syncwarp();
+      if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SFREE(q)));  // S buffer free for the next GEMM
+      lgp_mbar_wait(TBAR(TSB_SFULL(s)), (c / LGP_TC_STAGES) & 1);  // p chunk visible
+      const double* vj = reinterpret_cast<const double*>(stg + (size_t)s * TS_STAGE_BYTES + TC_B1_BYTES);
+      // columns of this chunk intersect the row block's diagonal: mask
+      const bool diag = chunk < 2 * I + 2;
+      const long long gj0 = (long long)chunk * TC_CH;
+      double* cb = cbuf + ((size_t)(w * 2 + (k & 1)) * 4 + q4) * TC_CH;
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        double cv[32];
+        if (!diag) {
+          // off-diagonal chunk: every entry feeds both sides
+#pragma unroll
+          for (int m = 0; m < 32; ++m) {
+            const int j = 32 * g + m;
+            const double kd = lgp_widen_nn(lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[j])), a, 0));
+            acc = fma(kd, vj[j], acc);
+            cv[m] = kd * vi;
+          }
+        } else {
+          // diagonal block: row side j >= i, column side j > i
+#pragma unroll
+          for (int m = 0; m < 32; ++m) {
+            const int j = 32 * g + m;
+            const long long gj = gj0 + j;
+            const float kk = lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[j])), a, 0);
+            acc = fma(lgp_widen_nn(gj >= gi ? kk : 0.f), vj[j], acc);
+            cv[m] = lgp_widen_nn(gj > gi ? kk : 0.f) * vi;
+          }
+        }
+        // transpose-reduce over the warp: after level o each lane keeps o
+        // partial columns; after 5 levels lane l holds column 32g + l
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int m = 0; m < o; ++m) {
+            const double send = up ? cv[m] : cv[m + o];
+            const double keep = up ? cv[m + o] : cv[m];
+            cv[m] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        cb[32 * g + lane] = cv[0];
+      }
+      __syncwarp();
+      if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SEMPTY(s)));  // p chunk read: stage reusable
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + w) : "memory");
+      // column partials of this (I, chunk): warps 0..3 in a fixed order
+      if (lane < 16) {
+        const int j = 16 * q4 + lane;
+        const double* b0 = cbuf + (size_t)(w * 2 + (k & 1)) * 4 * TC_CH;
+        const double sum = ((b0[j] + b0[TC_CH + j]) + b0[2 * TC_CH + j]) + b0[3 * TC_CH + j];
+        a.colpart[(size_t)(a.colbase[I] + chunk - 2 * I) * TC_CH + j] = sum;
+      }
+    }
+    // row partial of this segment: warpgroup 0 + warpgroup 1, fixed order
+    if (w == 1) comb[row] = acc;
+    asm volatile("bar.sync 3, 256;" ::: "memory");
+    if (w == 0) a.rowpart[(size_t)item * 128 + row] = acc + comb[row];
+  }
+  lgp_tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    lgp_tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+#undef TBAR
+#undef TS_SB
+}

@@ -94,7 +94,21 @@ void MatvecOp::prepare() {
       flags |= LGP_DIST_DIRECT;
     }
   }
-  if (allow_tc) plan = make_tc_plan(k->tree, rows->d, t, flags);
+  // the CG matvec (square operator, one RHS, one rank): symmetric tensor-core
+  // kernel, each unordered pair evaluated once, FP64 contraction with exact p.
+  // Opt-in (LGP_TCSYM=1): exactly symmetric (CG iteration counts match the
+  // SIMT kernel) but latency-bound in its FP64 column butterfly - 4.10 vs
+  // 4.21 ms on cfg4, slower on Matern trees (profiles/r01_tcsym.txt).
+  tcsym = false;
+  if (t == 1 && rows == cols && ctx->world == 1 && row0 == 0 && n_rows == rows->n &&
+      !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && std::getenv("LGP_TCSYM")) {
+    Plan p = make_tc_plan(k->tree, rows->d, 16, flags);
+    if (p.tc && !p.tc_pair) {
+      plan = p;
+      tcsym = true;
+    }
+  }
+  if (!tcsym && allow_tc) plan = make_tc_plan(k->tree, rows->d, t, flags);
   if (plan.tc) {
     tb = plan.tc_n;
   } else {
@@ -171,6 +185,41 @@ void MatvecOp::prepare() {
     LGP_CU_CHECK(drv::LaunchKernel(mod->prep, (unsigned)ceil_div<int64_t>(n_cols_pad, 128), 1, 1,
                                    128, 1, 1, 0, (CUstream)ctx->stream, p2, nullptr));
     ++ctx->launches;
+    if (tcsym) {
+      // work items: row block I x a segment of its column chunks [2I, n_tiles);
+      // column partial records (I, c) laid out block after block
+      int64_t total = 0;
+      for (int I = 0; I < n_rb; ++I) total += std::max(0, n_tiles - 2 * I);
+      const int S = (int)std::max<int64_t>(8, ceil_div<int64_t>(total, (int64_t)ctx->sm_count * 16));
+      std::vector<int> it, f0(n_rb), ns(n_rb);
+      std::vector<long long> cb(n_rb);
+      long long rec = 0;
+      for (int I = 0; I < n_rb; ++I) {
+        const int cs = 2 * I, m = std::max(0, n_tiles - cs);
+        cb[I] = rec;
+        f0[I] = (int)(it.size() / 3);
+        ns[I] = ceil_div(m, S);
+        for (int g = 0; g < ns[I]; ++g) {
+          it.push_back(I);
+          it.push_back(cs + g * S);
+          it.push_back(std::min(cs + (g + 1) * S, n_tiles));
+        }
+        rec += m;
+      }
+      n_items = (int)(it.size() / 3);
+      items = (int*)ctx->scratch_get(tag + ".items", it.size() * 4);
+      colbase = (long long*)ctx->scratch_get(tag + ".colbase", (size_t)n_rb * 8);
+      item0 = (int*)ctx->scratch_get(tag + ".item0", (size_t)n_rb * 2 * 4);
+      nsegb = item0 + n_rb;
+      // pageable sources: the copies complete before cudaMemcpyAsync returns
+      LGP_CUDA_CHECK(cudaMemcpyAsync(items, it.data(), it.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+      LGP_CUDA_CHECK(cudaMemcpyAsync(colbase, cb.data(), cb.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+      LGP_CUDA_CHECK(cudaMemcpyAsync(item0, f0.data(), f0.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+      LGP_CUDA_CHECK(cudaMemcpyAsync(nsegb, ns.data(), ns.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+      partial = (double*)ctx->scratch_get(tag + ".rowp", (size_t)n_items * 128 * 8);
+      colpart = (double*)ctx->scratch_get(tag + ".colp", (size_t)std::max<long long>(rec, 1) * 64 * 8);
+      vpack = (double*)ctx->scratch_get(tag + ".v", (size_t)std::max(n_rows_pad, n_cols_pad) * 8);
+    }
     return;
   }
   // symmetric block-pair kernel for the square operator on a single rank
@@ -242,6 +291,27 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     ctx->ev_pending.push_back(ev);
   };
   if (plan.tc) {
+    if (tcsym) {
+      const int npad = std::max(n_rows_pad, n_cols_pad);
+      vec::pack_rhs(ctx, V_dev, cols->n, 1, npad, 1, 1, vpack, done);
+      LgpTcSymArgs a;
+      std::memset(&a, 0, sizeof a);
+      a.a1 = fr;
+      a.b1 = fc;
+      a.v = vpack;
+      a.items = items;
+      a.colbase = colbase;
+      a.rowpart = partial;
+      a.colpart = colpart;
+      a.done = done;
+      std::memcpy(a.kc, plan.tca.kc, sizeof a.kc);
+      prof_begin();
+      launch(ctx, mod->tcsym, (unsigned)n_items, 1, 320, plan.smem_tcsym, &a);
+      prof_end();
+      vec::tcsym_epilogue(ctx, partial, colpart, item0, nsegb, colbase, n_rows, plan.root_scale,
+                          noise, noise_v, out_dev, done);
+      return;
+    }
     vec::pack_rhs_tc(ctx, V_dev, cols->n, t, n_tiles, tb, n_pass, vtc, vscale, v_inexact, done);
     LgpTcArgs a = plan.tca;
     a.v_inexact = v_inexact;

@@ -102,6 +102,7 @@ struct Plan {
   bool tc_pair = false;     // K1-TC on CTA pairs (cta_group::2, 256-row blocks)
   int tc_fw = 0;            // FP32 features per point for FMA-pipe distance chunks
   bool tc_simt = false;     // some K1-TC chunks compute distances on the FMA pipe
+  size_t smem_tcsym = 0;    // dynamic shared memory of lgp_matvec_tcsym
   LgpTcArgs tca{};          // kc[] filled
 };
 
@@ -122,6 +123,7 @@ struct Module {
   CUmodule mod = nullptr;
   CUfunction prep = nullptr, matvec = nullptr, gram = nullptr, diag = nullptr;
   CUfunction matvec_sym = nullptr;  // symmetric-operator K1 (SIMT modules)
+  CUfunction tcsym = nullptr;       // symmetric tensor-core K1, t = 1 (TC modules)
   bool tc = false;  // module holds lgp_tc_prep / lgp_matvec_tc in prep / matvec
   int blocks_per_sm = 1;
   int regs = 0;
@@ -212,6 +214,12 @@ struct MatvecOp {
   Module* mod = nullptr;
   bool allow_tc = false;  // may use the tensor-core K1 (matvec API, Lanczos; not CG)
   bool sym = false;       // square operator on one rank: symmetric block-pair kernel
+  bool tcsym = false;     // square operator, t = 1, one rank: symmetric tensor-core kernel
+  int n_items = 0;
+  int* items = nullptr;          // tcsym: [n_items][3]
+  long long* colbase = nullptr;  // tcsym: [n_rb]
+  int* item0 = nullptr;          // tcsym: [n_rb] first item / [n_rb] item count of each row block
+  int* nsegb = nullptr;
   int n_units = 0;
   int* units = nullptr;
   double* colpart = nullptr;
@@ -252,6 +260,11 @@ void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int 
 // UMMA K-major canonical layout
 void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int tbn, int n_pass,
                  void* out, float* scale, int* inexact, const int* done);
+// symmetric tensor-core K1 (t = 1): out_i = scale * (row partials of i's block
+// segments + column partials (I, chunk(i)) for I <= chunk(i) / 2) + noise * v_i
+void tcsym_epilogue(Context* c, const double* rowpart, const double* colpart, const int* item0,
+                    const int* nseg, const long long* colbase, int64_t n, double scale,
+                    double noise, const double* noise_v, double* out, const int* done);
 void epilogue(Context* c, const double* partial, int n_seg, int n_pass, int64_t rows_pad, int tb,
               int64_t n_rows, int t, double scale, double noise, const double* noise_v,
               double* out, const int* done);

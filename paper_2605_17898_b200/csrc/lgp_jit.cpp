@@ -171,6 +171,11 @@ Module* get_module(Context* ctx, const Plan& plan) {
   if (plan.tc) {
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->prep, m->mod, "lgp_tc_prep"));
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->matvec, m->mod, "lgp_matvec_tc"));
+    if (!plan.tc_pair) {
+      LGP_CU_CHECK(drv::ModuleGetFunction(&m->tcsym, m->mod, "lgp_matvec_tcsym"));
+      LGP_CU_CHECK(drv::FuncSetAttribute(m->tcsym, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                         (int)plan.smem_tcsym));
+    }
   } else {
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->prep, m->mod, "lgp_prep"));
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->matvec, m->mod, "lgp_matvec"));

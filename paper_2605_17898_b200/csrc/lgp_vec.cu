@@ -547,6 +547,28 @@ __global__ void k_pt_radius(const double* __restrict__ x, long long n, int d,
   if ((threadIdx.x & 31) == 0 && isfinite(m)) atomicMax(r2max, __double_as_longlong(m));
 }
 
+__global__ void k_tcsym_epilogue(const double* __restrict__ rowpart,
+                                 const double* __restrict__ colpart, const int* __restrict__ item0,
+                                 const int* __restrict__ nseg, const long long* __restrict__ colbase,
+                                 long long n, double scale, double noise,
+                                 const double* __restrict__ noise_v, double* __restrict__ out,
+                                 const int* done) {
+  if (is_done(done)) return;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int I = (int)(i >> 7), r = (int)(i & 127);
+    const long long c = i >> 6;
+    const int jj = (int)(i & 63);
+    double s = 0.0;
+    const int f = item0[I], m = nseg[I];
+    for (int k = 0; k < m; ++k) s += rowpart[(size_t)(f + k) * 128 + r];
+    for (long long I2 = 0; 2 * I2 <= c; ++I2) s += colpart[(size_t)(colbase[I2] + c - 2 * I2) * 64 + jj];
+    double o = __dmul_rn(scale, s);
+    if (noise_v != nullptr && noise != 0.0) o = __dadd_rn(o, __dmul_rn(noise, noise_v[i]));
+    out[i] = o;
+  }
+}
+
 inline int grid_for(long long total, int bd = 256) {
   long long g = (total + bd - 1) / bd;
   if (g > 148 * 16) g = 148 * 16;
@@ -596,6 +618,14 @@ void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int
   LGP_CUDA_CHECK(cudaMemsetAsync(inexact, 0, sizeof(int), c->stream));
   k_pack_tc<<<grid_for((long long)n_pass * n_tiles * tbn * 64), 256, 0, c->stream>>>(
       V, n, t, n_tiles, tbn, n_pass, scale, (__half*)out, inexact, done);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void tcsym_epilogue(Context* c, const double* rowpart, const double* colpart, const int* item0,
+                    const int* nseg, const long long* colbase, int64_t n, double scale,
+                    double noise, const double* noise_v, double* out, const int* done) {
+  k_tcsym_epilogue<<<grid_for(n), 256, 0, c->stream>>>(rowpart, colpart, item0, nseg, colbase, n,
+                                                       scale, noise, noise_v, out, done);
   LGP_LAUNCH_CHECK(c);
 }
 

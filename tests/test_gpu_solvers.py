@@ -125,3 +125,20 @@ def test_model_small_matrix_free_branch(gpu_ctx, name):
     assert np.max(np.abs(var - g[f"{name}_var"])) <= 3e-3
     lml = G.log_marginal_likelihood(st, seed=0)
     assert abs(lml - float(g[f"{name}_lml"])) <= 1e-4 * abs(float(g[f"{name}_lml"]))
+
+
+def test_symmetric_tensor_core_cg_opt_in(gpu_ctx, monkeypatch):
+    """The opt-in symmetric tensor-core CG matvec (LGP_TCSYM=1) evaluates each
+    unordered pair once: exactly symmetric, so CG matches the SIMT kernel's
+    iteration count and solution, and the matvec meets the 1e-5 bar."""
+    x, b = small_inputs(3000, 8, 41)
+    k = G.parse_kernel("(scale 1.2 (rbf 0.6))")
+    base = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
+    monkeypatch.setenv("LGP_TCSYM", "1")
+    op = G.KernelOperator(k, x, 0.1)
+    res = G.cg_solve(op, b, G.CgConfig(rel_tolerance=1e-8))
+    assert abs(res.iterations - base.iterations) <= max(2, 0.03 * base.iterations)
+    assert rel_l2(res.x, base.x) <= 1e-4
+    v = np.random.default_rng(5).standard_normal(3000)
+    ref = O.matvec(O.parse_tree(G.format_kernel(k)), x, 0.1, v)
+    assert rel_l2(op(v), ref) <= 1e-5
