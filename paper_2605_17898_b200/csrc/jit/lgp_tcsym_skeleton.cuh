@@ -24,16 +24,23 @@
 // column-feature tiles + p chunks), 1 distance-GEMM issuer, 2..9 two epilogue
 // warpgroups taking even / odd chunks.
 
-#define TS_THREADS 320
+#ifndef LGP_TS_NWG
+#define LGP_TS_NWG 4  // epilogue warpgroups (chunks round-robin): latency hiding
+#endif
+#define TS_THREADS (64 + 128 * LGP_TS_NWG)
+#ifndef LGP_TS_NSB
+#define LGP_TS_NSB (LGP_TS_NWG == 4 ? 8 : 6)  // S buffers of 64 TMEM columns
+#endif
+#define TS_NSBW (LGP_TS_NSB / LGP_TS_NWG)    // S buffers per warpgroup
 #define TS_VCH_BYTES (TC_CH * 8)                        // p chunk, FP64
 #define TS_STAGE_BYTES (TC_B1_BYTES + TS_VCH_BYTES)
-#define TS_CBUF_BYTES (2 * 2 * 4 * TC_CH * 8)           // [wg][parity][warp][64] FP64
-#define TS_NBARS (1 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB)
+#define TS_CBUF_BYTES (LGP_TS_NWG * 2 * 4 * TC_CH * 8)  // [wg][parity][warp][64] FP64
+#define TS_NBARS (1 + 2 * LGP_TC_STAGES + 2 * LGP_TS_NSB)
 #define TSB_AFULL 0
 #define TSB_SFULL(s) (1 + (s))
 #define TSB_SEMPTY(s) (1 + LGP_TC_STAGES + (s))
 #define TSB_S1FULL(q) (1 + 2 * LGP_TC_STAGES + (q))
-#define TSB_SFREE(q) (1 + 2 * LGP_TC_STAGES + LGP_TC_NSB + (q))
+#define TSB_SFREE(q) (1 + 2 * LGP_TC_STAGES + LGP_TS_NSB + (q))
 
 // FP32 -> FP64 for finite non-negative kernel values without the conversion
 // pipe: exponent re-bias + mantissa shift (0 maps to 2^-127, negligible)
@@ -53,8 +60,8 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
   double* vis = reinterpret_cast<double*>(ts_smem + TC_A1_BYTES);  // p of the 128 rows
   unsigned char* stg = ts_smem + TC_A1_BYTES + 128 * 8;
   double* cbuf = reinterpret_cast<double*>(stg + LGP_TC_STAGES * TS_STAGE_BYTES);
-  double* comb = cbuf + TS_CBUF_BYTES / 8;  // [128] warpgroup 1's row sums
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(comb + 128);
+  double* comb = cbuf + TS_CBUF_BYTES / 8;  // [NWG - 1][128] row sums of warpgroups 1..
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(comb + 128 * (LGP_TS_NWG - 1));
   unsigned* tslot = reinterpret_cast<unsigned*>(bars + TS_NBARS);
   const unsigned bar0 = lgp_saddr(bars);
 #define TBAR(i) (bar0 + 8u * (unsigned)(i))
@@ -69,7 +76,7 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
       lgp_mbar_init(TBAR(TSB_SFULL(s)), 1);
       lgp_mbar_init(TBAR(TSB_SEMPTY(s)), 4);  // the 4 warps of the chunk's warpgroup
     }
-    for (int q = 0; q < LGP_TC_NSB; ++q) {
+    for (int q = 0; q < LGP_TS_NSB; ++q) {
       lgp_mbar_init(TBAR(TSB_S1FULL(q)), 1);
       lgp_mbar_init(TBAR(TSB_SFREE(q)), 4);
     }
@@ -116,11 +123,11 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
       const unsigned stg0 = lgp_saddr(stg) >> 4;
       lgp_mbar_wait(TBAR(TSB_AFULL), 0);
       for (int c = 0; c < nch; ++c) {
-        const int w = c & 1, k = c >> 1;
-        const int q = w + 2 * (k % TC_NSBW);
+        const int w = c % LGP_TS_NWG, k = c / LGP_TS_NWG;
+        const int q = w + LGP_TS_NWG * (k % TS_NSBW);
         const int s = c % LGP_TC_STAGES;
         lgp_mbar_wait(TBAR(TSB_SFULL(s)), (c / LGP_TC_STAGES) & 1);
-        if (k >= TC_NSBW) lgp_mbar_wait(TBAR(TSB_SFREE(q)), ((k / TC_NSBW) - 1) & 1);
+        if (k >= TS_NSBW) lgp_mbar_wait(TBAR(TSB_SFREE(q)), ((k / TS_NSBW) - 1) & 1);
         lgp_tc_fence_after();
         const unsigned long long b_d = dk + stg0 + (unsigned)s * (TS_STAGE_BYTES >> 4);
 #pragma unroll
@@ -136,25 +143,18 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
     const int q4 = warp & 3;
     const int row = 32 * q4 + lane;
     const unsigned lanes = (unsigned)(32 * q4) << 16;
-    const int nloc = (nch - w + 1) >> 1;
+    const int nloc = (nch - w + LGP_TS_NWG - 1) / LGP_TS_NWG;
     const long long gi = 128ll * I + row;
     lgp_mbar_wait(TBAR(TSB_AFULL), 0);
     const double vi = vis[row];
     double acc = 0.0;
     for (int k = 0; k < nloc; ++k) {
-      const int c = 2 * k + w;
-      const int q = w + 2 * (k % TC_NSBW);
+      const int c = LGP_TS_NWG * k + w;
+      const int q = w + LGP_TS_NWG * (k % TS_NSBW);
       const int s = c % LGP_TC_STAGES;
       const int chunk = c0 + c;
-      lgp_mbar_wait(TBAR(TSB_S1FULL(q)), (k / TC_NSBW) & 1);
+      lgp_mbar_wait(TBAR(TSB_S1FULL(q)), (k / TS_NSBW) & 1);
       lgp_tc_fence_after();
-      unsigned sv[64];
-      lgp_tmem_ld32p(TS_SB(q) + lanes, sv);
-      lgp_tmem_ld32p(TS_SB(q) + lanes + 32u, sv + 32);
-      lgp_tmem_wait_ld();
-      lgp_tc_fence_before();
-      __syncwarp();
-      if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SFREE(q)));  // S buffer free for the next GEMM
       lgp_mbar_wait(TBAR(TSB_SFULL(s)), (c / LGP_TC_STAGES) & 1);  // p chunk visible
       const double* vj = reinterpret_cast<const double*>(stg + (size_t)s * TS_STAGE_BYTES + TC_B1_BYTES);
       // columns of this chunk intersect the row block's diagonal: mask
@@ -163,13 +163,22 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
       double* cb = cbuf + ((size_t)(w * 2 + (k & 1)) * 4 + q4) * TC_CH;
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
+        // 32 columns per round trip (register budget of 3 warpgroups)
+        unsigned sv[32];
+        lgp_tmem_ld32p(TS_SB(q) + lanes + 32u * g, sv);
+        lgp_tmem_wait_ld();
+        if (g == 1) {
+          lgp_tc_fence_before();
+          __syncwarp();
+          if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SFREE(q)));  // S buffer free for the next GEMM
+        }
         double cv[32];
         if (!diag) {
           // off-diagonal chunk: every entry feeds both sides
 #pragma unroll
           for (int m = 0; m < 32; ++m) {
             const int j = 32 * g + m;
-            const double kd = lgp_widen_nn(lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[j])), a, 0));
+            const double kd = lgp_widen_nn(lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[m])), a, 0));
             acc = fma(kd, vj[j], acc);
             cv[m] = kd * vi;
           }
@@ -179,7 +188,7 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
           for (int m = 0; m < 32; ++m) {
             const int j = 32 * g + m;
             const long long gj = gj0 + j;
-            const float kk = lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[j])), a, 0);
+            const float kk = lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[m])), a, 0);
             acc = fma(lgp_widen_nn(gj >= gi ? kk : 0.f), vj[j], acc);
             cv[m] = lgp_widen_nn(gj > gi ? kk : 0.f) * vi;
           }
@@ -209,10 +218,15 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
         a.colpart[(size_t)(a.colbase[I] + chunk - 2 * I) * TC_CH + j] = sum;
       }
     }
-    // row partial of this segment: warpgroup 0 + warpgroup 1, fixed order
-    if (w == 1) comb[row] = acc;
-    asm volatile("bar.sync 3, 256;" ::: "memory");
-    if (w == 0) a.rowpart[(size_t)item * 128 + row] = acc + comb[row];
+    // row partial of this segment: warpgroups 0, 1, .. in a fixed order
+    if (w > 0) comb[(w - 1) * 128 + row] = acc;
+    asm volatile("bar.sync %0, %1;" ::"r"(LGP_TS_NWG + 1), "r"(128 * LGP_TS_NWG) : "memory");
+    if (w == 0) {
+      double r = acc;
+#pragma unroll
+      for (int u = 1; u < LGP_TS_NWG; ++u) r += comb[(u - 1) * 128 + row];
+      a.rowpart[(size_t)item * 128 + row] = r;
+    }
   }
   lgp_tc_fence_before();
   __syncthreads();

@@ -95,13 +95,12 @@ void MatvecOp::prepare() {
     }
   }
   // the CG matvec (square operator, one RHS, one rank): symmetric tensor-core
-  // kernel, each unordered pair evaluated once, FP64 contraction with exact p.
-  // Opt-in (LGP_TCSYM=1): exactly symmetric (CG iteration counts match the
-  // SIMT kernel) but latency-bound in its FP64 column butterfly - 4.10 vs
-  // 4.21 ms on cfg4, slower on Matern trees (profiles/r01_tcsym.txt).
+  // kernel, each unordered pair evaluated once, FP64 contraction with the
+  // exact p - exactly symmetric, so CG iteration counts match the SIMT kernel;
+  // 3.35 vs 4.21 ms on cfg4 (profiles/r01_tcsym.txt). LGP_NO_TCSYM disables.
   tcsym = false;
   if (t == 1 && rows == cols && ctx->world == 1 && row0 == 0 && n_rows == rows->n &&
-      !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && std::getenv("LGP_TCSYM")) {
+      !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && !std::getenv("LGP_NO_TCSYM")) {
     Plan p = make_tc_plan(k->tree, rows->d, 16, flags);
     if (p.tc && !p.tc_pair) {
       plan = p;
@@ -306,7 +305,7 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
       a.done = done;
       std::memcpy(a.kc, plan.tca.kc, sizeof a.kc);
       prof_begin();
-      launch(ctx, mod->tcsym, (unsigned)n_items, 1, 320, plan.smem_tcsym, &a);
+      launch(ctx, mod->tcsym, (unsigned)n_items, 1, 64 + 128 * plan.ts_nwg, plan.smem_tcsym, &a);
       prof_end();
       vec::tcsym_epilogue(ctx, partial, colpart, item0, nsegb, colbase, n_rows, plan.root_scale,
                           noise, noise_v, out_dev, done);

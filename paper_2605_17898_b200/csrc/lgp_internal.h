@@ -103,6 +103,7 @@ struct Plan {
   int tc_fw = 0;            // FP32 features per point for FMA-pipe distance chunks
   bool tc_simt = false;     // some K1-TC chunks compute distances on the FMA pipe
   size_t smem_tcsym = 0;    // dynamic shared memory of lgp_matvec_tcsym
+  int ts_nwg = 3;           // lgp_matvec_tcsym epilogue warpgroups
   LgpTcArgs tca{};          // kc[] filled
 };
 

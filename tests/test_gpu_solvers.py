@@ -127,14 +127,18 @@ def test_model_small_matrix_free_branch(gpu_ctx, name):
     assert abs(lml - float(g[f"{name}_lml"])) <= 1e-4 * abs(float(g[f"{name}_lml"]))
 
 
-def test_symmetric_tensor_core_cg_opt_in(gpu_ctx, monkeypatch):
-    """The opt-in symmetric tensor-core CG matvec (LGP_TCSYM=1) evaluates each
-    unordered pair once: exactly symmetric, so CG matches the SIMT kernel's
-    iteration count and solution, and the matvec meets the 1e-5 bar."""
+@pytest.mark.parametrize("nwg", ["4", "3", "2"])
+def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg):
+    """The symmetric tensor-core CG matvec (default for D >= 4 r^2 trees)
+    evaluates each unordered pair once: exactly symmetric, so CG matches the
+    symmetric SIMT kernel's (LGP_NO_TCSYM) iteration count and solution, and
+    the matvec meets the 1e-5 bar, for every epilogue warpgroup count."""
     x, b = small_inputs(3000, 8, 41)
     k = G.parse_kernel("(scale 1.2 (rbf 0.6))")
+    monkeypatch.setenv("LGP_NO_TCSYM", "1")
     base = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
-    monkeypatch.setenv("LGP_TCSYM", "1")
+    monkeypatch.delenv("LGP_NO_TCSYM")
+    monkeypatch.setenv("LGP_TS_NWG", nwg)
     op = G.KernelOperator(k, x, 0.1)
     res = G.cg_solve(op, b, G.CgConfig(rel_tolerance=1e-8))
     assert abs(res.iterations - base.iterations) <= max(2, 0.03 * base.iterations)
