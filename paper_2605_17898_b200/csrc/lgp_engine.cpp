@@ -60,6 +60,10 @@ void* Context::scratch_get(const std::string& name, size_t bytes) {
 }
 
 namespace {
+// scratch budget of the symmetric kernels' partials; larger operators use the
+// plain row-block kernels (partials O(N) per column segment)
+constexpr double kSymPartialBudget = 16.0 * (1ull << 30);
+
 int pick_tb(int t) {
   if (t >= 16) return 16;
   int tb = 1;
@@ -99,7 +103,11 @@ void MatvecOp::prepare() {
   // exact p - exactly symmetric, so CG iteration counts match the SIMT kernel;
   // 3.35 vs 4.21 ms on cfg4 (profiles/r01_tcsym.txt). LGP_NO_TCSYM disables.
   tcsym = false;
+  // column partials: one 64-column record per (row block, chunk) pair, n^2/8192
+  // records of 512 B - bounded (N <= ~1.1M) so they fit comfortably in HBM
+  const double tcsym_bytes = (double)rows->n * (double)rows->n / 8192.0 * 512.0;
   if (t == 1 && rows == cols && ctx->world == 1 && row0 == 0 && n_rows == rows->n &&
+      tcsym_bytes <= kSymPartialBudget &&
       !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && !std::getenv("LGP_NO_TCSYM")) {
     Plan p = make_tc_plan(k->tree, rows->d, 16, flags);
     if (p.tc && !p.tc_pair) {
@@ -222,8 +230,10 @@ void MatvecOp::prepare() {
     return;
   }
   // symmetric block-pair kernel for the square operator on a single rank
+  // block-pair partials: 2 x rows_per_cta FP64 per unit, n_rb^2 / 2 units
+  const double sym_bytes = (double)n_rb * (n_rb + 1) / 2.0 * rows_per_cta * 16.0 * n_pass * tb;
   sym = (rows == cols) && ctx->world == 1 && tb == 1 && !(flags & LGP_NO_SYM) &&
-        (rows_per_cta % tu.cc) == 0 && n_rb >= 2;
+        (rows_per_cta % tu.cc) == 0 && n_rb >= 2 && sym_bytes <= kSymPartialBudget;
   if (sym) {
     n_cols_pad = n_rows_pad;  // column blocks = row blocks
     n_tiles = n_cols_pad / tu.cc;
