@@ -104,6 +104,7 @@
 #error "FMA-pipe distance chunks are single-CTA only"
 #endif
 #define TC_SIMT(c) ((LGP_TC_SIMT_MASK >> ((c) & 7)) & 1)
+#define TC_HMMA_CHUNK(c) ((LGP_TC_HMMA >> ((c) & 7)) & 1)
 #define TC_COMB_BYTES (128 * LGP_TC_N * 8)
 #ifndef LGP_TC_NSB
 #define LGP_TC_NSB 6   // S buffers in TMEM (64 columns each), even: NSB/2 per warpgroup
@@ -404,6 +405,40 @@ __device__ __forceinline__ void lgp_tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// ---- warp-level tensor-core distance tile (LGP_TC_HMMA): mma.sync keeps -r^2
+// in registers, so no tcgen05.ld of an FP32 S tile is needed
+// LGP_TC_HMMA: mask over c % 8 of the chunks that take this path (0xFF = all)
+#ifndef LGP_TC_HMMA
+#define LGP_TC_HMMA 0
+#endif
+__device__ __forceinline__ void lgp_ldsm_x4(unsigned addr, unsigned (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void lgp_ldsm_x2(unsigned addr, unsigned& r0, unsigned& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(addr));
+}
+__device__ __forceinline__ void lgp_hmma(float (&c)[4], const unsigned (&a)[4], unsigned b0,
+                                         unsigned b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// 16 lanes x 32 columns from the m16n8 accumulator layout: register 2r holds
+// (lane t/4, column 4r + t%4), register 2r + 1 (lane t/4 + 8, same column)
+__device__ __forceinline__ void lgp_tmem_st16x128_x8(unsigned taddr, const unsigned (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x128b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16};" ::"r"(taddr),
+      LGP_W8(v, 0), LGP_W8(v, 8)
+      : "memory");
+}
+
 // FP16 hi/lo split of two FP32 values, packed {lo half = x0, hi half = x1}:
 // hi = RN(x), lo = RN(x - hi) with x - hi formed exactly by the mixed-precision
 // FMA (FHFMA: FP16 operand, FP32 addend), no FP16 -> FP32 unpack needed
@@ -623,7 +658,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 11 && rank == 0) {
-    if (lane == 0) {
+    if (lane == 0 && LGP_TC_HMMA != 0xFF) {
       // -------------------------------------- distance-GEMM issuer (leader)
       // every chunk in order, once it is staged (in both CTAs of a pair) and
       // its S buffer's previous contraction has completed (PEMPTY)
@@ -634,7 +669,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
 #endif
       TR_DECL
       for (int c = 0; c < nch; ++c) {
-        if (TC_SIMT(c)) continue;  // distances of this chunk come from the FMA pipe
+        if (TC_SIMT(c) || TC_HMMA_CHUNK(c)) continue;  // distances from the FMA pipe / mma.sync
         const int w = c & 1, k = c >> 1;
         const int q = w + 2 * (k % TC_NSBW);
         const int s = c % LGP_TC_STAGES;
@@ -723,6 +758,21 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
     double acc[LGP_TC_N];
 #pragma unroll
     for (int i = 0; i < LGP_TC_N; ++i) acc[i] = 0.0;
+#if LGP_TC_HMMA
+    // A fragments of this warp's 32 rows (2 m16 tiles x KD/16 k-steps), once
+    lgp_mbar_wait(BAR(B_AFULL), 0);
+    unsigned af[2][LGP_TC_KD / 16][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int ks = 0; ks < LGP_TC_KD / 16; ++ks) {
+        const int mi = lane >> 3;
+        const int r = 32 * q4 + 16 * mt + (mi & 1) * 8 + (lane & 7);
+        const int kc = 2 * ks + (mi >> 1);
+        lgp_ldsm_x4(lgp_saddr(a1s) + (unsigned)((r >> 3) * (LGP_TC_KD * 16) + kc * 128 + (r & 7) * 16),
+                    af[mt][ks]);
+      }
+#endif
 #if LGP_TC_SIMT_MASK
     float rf32[LGP_D + 1];  // this thread's row: (c_i, -|c_i|^2)
 #pragma unroll
@@ -754,6 +804,59 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int k = 0; k < nloc; ++k) {
       const int q = w + 2 * (k % TC_NSBW);
       const unsigned sb = T_SB(q) + lanes;
+#if LGP_TC_HMMA
+      if (TC_HMMA_CHUNK(2 * k + w)) {
+        // -r^2 of this warp's 32 rows x 64 columns by mma.sync (FP32 in
+        // registers), straight into the tree and the FP16 hi/lo split; P goes to
+        // TMEM in the accumulator layout (tcgen05.st 16x128b), no S round trip
+        const int c = 2 * k + w;
+        const int st = c % LGP_TC_STAGES;
+        lgp_mbar_wait(BAR(B_SFULL(st)), (c / LGP_TC_STAGES) & 1);  // column features staged
+        if (k >= TC_NSBW) lgp_mbar_wait(BAR(B_PEMPTY(q)), ((k / TC_NSBW) - 1) & 1);  // P buffer free
+        if (lane == 0) { TR_MARK(9) }
+        lgp_tc_fence_after();
+        const unsigned b1s = lgp_saddr(stg + (size_t)st * TC_STAGE_BYTES);
+        float cf[2][8][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) cf[mt][nt][e] = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+          for (int ks = 0; ks < LGP_TC_KD / 16; ++ks) {
+            const int nrow = 8 * nt + (lane & 7);
+            const int kc = 2 * ks + ((lane >> 3) & 1);
+            unsigned b0, b1;
+            lgp_ldsm_x2(b1s + (unsigned)((nrow >> 3) * (LGP_TC_KD * 16) + kc * 128 + (nrow & 7) * 16),
+                        b0, b1);
+            lgp_hmma(cf[0][nt], af[0][ks], b0, b1);
+            lgp_hmma(cf[1][nt], af[1][ks], b0, b1);
+          }
+        unsigned hw[2][16], lw[2][16];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt) {
+            const int px = nt < (LGP_TC_POLY + 1) / 2 ? 1 : 0;
+            const int px1 = nt < LGP_TC_POLY / 2 ? 1 : 0;
+            float kv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              kv[e] = lgp_tc_k(LGP_TC_CLAMP(cf[mt][nt][e]), a, (e & 1) ? px1 : px);
+            lgp_split_f16x2(kv[0], kv[1], hw[mt][2 * nt], lw[mt][2 * nt]);
+            lgp_split_f16x2(kv[2], kv[3], hw[mt][2 * nt + 1], lw[mt][2 * nt + 1]);
+          }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          lgp_tmem_st16x128_x8(sb + ((16u * mt) << 16), hw[mt]);        // hi pairs: columns 0..31
+          lgp_tmem_st16x128_x8(sb + ((16u * mt) << 16) + 32u, lw[mt]);  // lo pairs: columns 32..63
+        }
+      } else
+#endif
+      {
       unsigned s[64];
       if (lane == 0) { TR_MARK(8) }
 #if LGP_TC_SIMT_MASK
@@ -809,6 +912,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       lgp_tmem_st32s2(sb, s);        // hi pairs -> columns 0..31
       lgp_tmem_st32s2(sb + 32u, s + 1);  // lo pairs -> columns 32..63
+      }
       lgp_tmem_wait_st();
       lgp_tc_fence_before();
       __syncwarp();
