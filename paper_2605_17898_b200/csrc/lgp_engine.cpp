@@ -347,7 +347,10 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     }
     a.trace = trace;
     prof_begin();
-    launch(ctx, mod->matvec, (unsigned)grid, 1, plan.tune.threads, plan.smem_bytes, &a);
+    if (plan.tc_v5)
+      launch(ctx, mod->tc4, (unsigned)grid, 1, 96 + 128 * plan.t4_nwg, plan.smem_tc4, &a);
+    else
+      launch(ctx, mod->matvec, (unsigned)grid, 1, plan.tune.threads, plan.smem_bytes, &a);
     prof_end();
     if (trace) {
       unsigned long long h[16];

@@ -104,6 +104,9 @@ struct Plan {
   bool tc_simt = false;     // some K1-TC chunks compute distances on the FMA pipe
   size_t smem_tcsym = 0;    // dynamic shared memory of lgp_matvec_tcsym
   int ts_nwg = 3;           // lgp_matvec_tcsym epilogue warpgroups
+  bool tc_v5 = false;       // use lgp_matvec_tc4 (mma.sync distance tiles) for t > 1
+  int t4_nwg = 4;
+  size_t smem_tc4 = 0;
   LgpTcArgs tca{};          // kc[] filled
 };
 
@@ -125,6 +128,7 @@ struct Module {
   CUfunction prep = nullptr, matvec = nullptr, gram = nullptr, diag = nullptr;
   CUfunction matvec_sym = nullptr;  // symmetric-operator K1 (SIMT modules)
   CUfunction tcsym = nullptr;       // symmetric tensor-core K1, t = 1 (TC modules)
+  CUfunction tc4 = nullptr;         // K1-TC with mma.sync distance tiles (TC modules)
   bool tc = false;  // module holds lgp_tc_prep / lgp_matvec_tc in prep / matvec
   int blocks_per_sm = 1;
   int regs = 0;

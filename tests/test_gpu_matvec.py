@@ -336,10 +336,13 @@ def test_results_in_pinned_buffers_survive(gpu_ctx):
 
 
 @pytest.mark.parametrize("env", [{"LGP_TC_PAIR": "1"}, {"LGP_TC_SIMT_MASK": "0x48"},
-                                 {"LGP_TC_POLY": "0"}, {"LGP_TC_G": "2", "LGP_TC_DLAG": "1"}])
+                                 {"LGP_TC_POLY": "0"}, {"LGP_TC_G": "2", "LGP_TC_DLAG": "1"},
+                                 {"LGP_TC_HMMA": "0x88"}, {"LGP_TC_V5": "1"},
+                                 {"LGP_TC_V5": "1", "LGP_T4_NWG": "3"}])
 def test_tensor_core_variants_parity(gpu_ctx, monkeypatch, env):
-    """The opt-in K1-TC variants (CTA pairs with cta_group::2, FMA-pipe distance
-    chunks, MUFU-only exp2, other drain schedules) meet the same bar."""
+    """The opt-in K1-TC variants (CTA pairs with cta_group::2, FMA-pipe or
+    mma.sync distance tiles, the mma.sync v5 kernel, MUFU-only exp2, other
+    drain schedules) meet the same bar."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     expr = "(+ (scale 2.0 (rbf 0.4)) (scale 0.5 (matern32 0.9)))"
