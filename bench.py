@@ -203,6 +203,13 @@ def run_reference(args, rank, world):
     nodes = O.parse_tree(cfg["kernel"])
     rows = 64 if cfg["n"] >= 50_000 else min(cfg["n"], 512)
     times = []
+    # rank 0 runs alone: give the BLAS all host cores (torchrun sets OMP_NUM_THREADS=1)
+    try:
+        import threadpoolctl
+
+        limiter = threadpoolctl.threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        limiter = None
     for s in range(args.warmup + args.steps):
         r0 = (s * 997 * rows) % max(cfg["n"] - rows, 1)
         t0 = time.perf_counter()
