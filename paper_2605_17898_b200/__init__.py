@@ -58,9 +58,14 @@ from .models import (
     DENSE_OPERATOR_MAX,
     FIT_CG_TOLERANCE,
     ExactState,
+    OptimizerConfig,
+    exact_evidence_objective,
+    flatten_model_params,
     gp_fit,
     gp_predict,
     log_marginal_likelihood,
+    optimize_hyperparams,
+    unflatten_model_params,
 )
 
 __all__ = [name for name in dir() if not name.startswith("_")]

@@ -147,3 +147,114 @@ def log_marginal_likelihood(state, seed=0):
     cfg = state.cg_config if state.cg_config is not None else CgConfig()
     ld = slq_logdet(_operator(state), n, cfg, seed=seed)
     return -0.5 * (quad + ld + n * LOG_2PI)
+
+
+# ------------------------------------------- hyper-parameter optimisation
+# (the caller of the fit + evidence path). Host-side
+# restatement of minigp/models.py:89-111 and :347-413; every objective
+# evaluation runs the device fit (lgp_cg) and SLQ evidence (lgp_lanczos).
+
+@dataclass
+class OptimizerConfig:
+    """Adam on central finite differences (models.py:89-111). `evaluations`
+    is written by optimize_hyperparams: steps * (2P + 1) calls."""
+
+    steps: int = 100
+    learning_rate: float = 0.05
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    fd_epsilon: float = 1e-4
+    evaluations: int = 0
+
+    def __post_init__(self):
+        if self.steps < 0:
+            raise ValueError("steps must be nonnegative")
+        if min(self.learning_rate, self.fd_epsilon, self.eps) <= 0:
+            raise ValueError("learning_rate, fd_epsilon and eps must be positive")
+        if not (0 < self.beta1 < 1 and 0 < self.beta2 < 1):
+            raise ValueError("beta coefficients must lie in (0, 1)")
+
+
+def flatten_model_params(kernel, noise):
+    """Log-space vector [kernel hyperparameters..., log noise] (models.py:347-349)."""
+    from .kernels import flatten_params
+
+    return tracked(np.append(flatten_params(kernel), math.log(noise)))
+
+
+def unflatten_model_params(kernel, values):
+    """(kernel, noise) from a flatten_model_params vector (models.py:352-359)."""
+    from .kernels import n_params, unflatten_params
+
+    values = np.asarray(values, dtype=np.float64)
+    want = n_params(kernel) + 1
+    if values.shape != (want,):
+        raise DimensionMismatchError(f"expected {want} values, got {values.shape}")
+    return unflatten_params(kernel, values[:-1]), float(np.exp(values[-1]))
+
+
+def optimize_hyperparams(objective, p0, config):
+    """Maximise `objective` over a log-space vector (models.py:362-413).
+
+    Adam ascent on a central-difference gradient: per step one centre call and
+    two per coordinate (2P + 1). A non-finite value stops the run; returns the
+    best centre seen and the trace of centre values.
+    """
+    p = np.array(p0, dtype=np.float64, copy=True)
+    if p.ndim != 1:
+        raise DimensionMismatchError("parameter vector must be 1-d")
+    config.evaluations = 0
+
+    def call(q):
+        config.evaluations += 1
+        return float(objective(q))
+
+    dim = p.shape[0]
+    m1 = np.zeros(dim)
+    m2 = np.zeros(dim)
+    trace, best_p, best = [], p.copy(), -np.inf
+    h = config.fd_epsilon
+    for step in range(1, config.steps + 1):
+        centre = call(p)
+        if not math.isfinite(centre):
+            break
+        trace.append(centre)
+        if centre > best:
+            best, best_p = centre, p.copy()
+        grad = np.empty(dim)
+        ok = True
+        for i in range(dim):
+            q = p.copy()
+            q[i] += h
+            up = call(q)
+            q[i] = p[i] - h
+            down = call(q)
+            if not (math.isfinite(up) and math.isfinite(down)):
+                ok = False
+                break
+            grad[i] = (up - down) / (2.0 * h)
+        if not ok:
+            break
+        m1 = config.beta1 * m1 + (1.0 - config.beta1) * grad
+        m2 = config.beta2 * m2 + (1.0 - config.beta2) * grad * grad
+        m1_hat = m1 / (1.0 - config.beta1**step)
+        m2_hat = m2 / (1.0 - config.beta2**step)
+        p = p + config.learning_rate * m1_hat / (np.sqrt(m2_hat) + config.eps)
+    return tracked(best_p), trace
+
+
+def exact_evidence_objective(x, y, kernel, cg_config=None, seed=0):
+    """q -> log marginal likelihood of gp_fit(x, y, *unflatten_model_params(
+    kernel, q), "cg"): the exact-GP objective for optimize_hyperparams, each
+    call one device CG fit and one device SLQ evidence. X is uploaded per call
+    (the kernel program is cached by tree shape, parameters are launch args)."""
+    x = as_matrix(x, "X")
+    y = as_vector(y, "y")
+
+    def objective(q):
+        k, noise = unflatten_model_params(kernel, q)
+        st = gp_fit(x, y, k, noise, "cg", cg_config=cg_config)
+        return log_marginal_likelihood(st, seed=seed)
+
+    return objective

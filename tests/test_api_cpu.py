@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import paper_2605_17898_b200 as G
+from conftest import golden
 from paper_2605_17898_b200 import kernels as K
 
 
@@ -188,3 +189,41 @@ def test_threaded_finite_scan_matches_numpy():
     b[8] = -np.finfo(np.float64).tiny / 2  # subnormal
     assert _lib.all_finite(b)
     assert _lib.all_finite(np.empty(0))
+
+
+def test_optimizer_matches_reference_bitwise():
+    """optimize_hyperparams (models.py:362-413) is host logic: the reference's
+    best point, centre trace and evaluation count on an analytic objective are
+    reproduced exactly; flatten / unflatten_model_params likewise."""
+    import math as _m
+
+    g = golden("optimizer.npz")
+
+    def toy(q):
+        c = np.array([0.3, -1.2, 0.8])
+        w = np.array([1.0, 0.5, 2.0])
+        return float(-np.sum(w * (q - c) ** 2) + 0.1 * _m.sin(3.0 * q[0]) - 0.05 * q[1] * q[2])
+
+    cfg = G.OptimizerConfig(steps=30, learning_rate=0.1)
+    best, trace = G.optimize_hyperparams(toy, np.zeros(3), cfg)
+    np.testing.assert_array_equal(best, g["toy_best"])
+    np.testing.assert_array_equal(np.array(trace), g["toy_trace"])
+    assert cfg.evaluations == int(g["toy_evals"]) == 30 * 7
+    k = G.parse_kernel("(+ (scale 1.3 (rbf 0.6)) (matern52 0.9))")
+    flat = G.flatten_model_params(k, 0.2)
+    np.testing.assert_array_equal(flat, g["flat_values"])
+    k2, noise2 = G.unflatten_model_params(k, flat + 0.1)
+    assert G.format_kernel(k2) == str(g["flat_kernel2"]) and noise2 == float(g["flat_noise2"])
+    with pytest.raises(G.DimensionMismatchError):
+        G.unflatten_model_params(k, flat[:2])
+    with pytest.raises(ValueError):
+        G.OptimizerConfig(beta1=1.0)
+    # a non-finite objective stops the run and returns the best point so far
+    calls = []
+
+    def bad(q):
+        calls.append(1)
+        return -float(np.sum(q * q)) if len(calls) < 5 else float("nan")
+
+    best, trace = G.optimize_hyperparams(bad, np.ones(2), G.OptimizerConfig(steps=10))
+    assert len(trace) == 1 and np.array_equal(best, np.ones(2))

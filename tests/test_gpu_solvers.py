@@ -146,3 +146,20 @@ def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg):
     v = np.random.default_rng(5).standard_normal(3000)
     ref = O.matvec(O.parse_tree(G.format_kernel(k)), x, 0.1, v)
     assert rel_l2(op(v), ref) <= 1e-5
+
+
+def test_evidence_optimizer_matches_reference(gpu_ctx):
+    """3 Adam steps of central-difference ascent on the exact-GP evidence
+    (every evaluation a device CG fit + device SLQ) track the reference's own
+    run (dense CG operator, SLQ seed 0) - the §8f caller of the fit path."""
+    g = golden("optimizer.npz")
+    rng = np.random.default_rng(17)
+    x = rng.random((600, 3))
+    y = np.sin(2.0 * x.sum(1)) + 0.1 * rng.standard_normal(600)
+    kernel = G.parse_kernel("(scale 1.0 (rbf 0.5))")
+    cfg = G.OptimizerConfig(steps=3, learning_rate=0.05)
+    obj = G.exact_evidence_objective(x, y, kernel, seed=0)
+    best, trace = G.optimize_hyperparams(obj, G.flatten_model_params(kernel, 0.1), cfg)
+    assert cfg.evaluations == int(g["gp_evals"]) == 21
+    np.testing.assert_allclose(np.array(trace), g["gp_trace"], rtol=1e-4)
+    np.testing.assert_allclose(best, g["gp_best"], atol=2e-3)
