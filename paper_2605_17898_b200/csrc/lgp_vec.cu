@@ -519,14 +519,20 @@ __global__ void k_pt_colsum(const double* __restrict__ x, long long n, int d, lo
   if (nf) atomicOr(bad, 1);
 }
 
+// one warp per column: lane-strided partial sums, then a fixed butterfly
+// (deterministic order)
 __global__ void k_pt_center(const double* __restrict__ part, int nblk, int d, long long n,
                             double* ctr, double* stats) {
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int j = threadIdx.x >> 5; j < d; j += blockDim.x >> 5) {
     double acc = 0.0;
-    for (int b = 0; b < nblk; ++b) acc += part[(long long)b * d + j];
-    const double c = n > 0 ? acc / (double)n : 0.0;
-    ctr[j] = c;
-    stats[j] = c;
+    for (int b = lane; b < nblk; b += 32) acc += part[(long long)b * d + j];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const double c = n > 0 ? acc / (double)n : 0.0;
+      ctr[j] = c;
+      stats[j] = c;
+    }
   }
 }
 
@@ -656,7 +662,7 @@ void point_stats(Context* c, const double* x, int64_t n, int d, double* ctr, dou
     k_pt_colsum<<<dim3(nblk, d), 256, 0, c->stream>>>(x, n, d, rows, scratch, bad);
     LGP_LAUNCH_CHECK(c);
   }
-  k_pt_center<<<1, 128, 0, c->stream>>>(scratch, n > 0 ? nblk : 0, d, n, ctr, stats);
+  k_pt_center<<<1, 512, 0, c->stream>>>(scratch, n > 0 ? nblk : 0, d, n, ctr, stats);
   LGP_LAUNCH_CHECK(c);
   if (n > 0) {
     k_pt_radius<<<grid_for(n), 256, 0, c->stream>>>(
