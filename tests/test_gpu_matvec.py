@@ -223,6 +223,7 @@ def test_reference_kernel_objects_are_accepted(gpu_ctx):
 # ---- tensor-core K1 (tcgen05, FP16x2 distance GEMM + FP16 hi/lo contraction)
 TC_CASES = [("(rbf 0.5)", 300, 8, 16), ("(rbf 0.5)", 1000, 8, 16), ("(matern52 0.7)", 777, 4, 8),
             ("(rbf 0.3)", 2000, 8, 16), ("(matern32 0.6)", 1500, 12, 16), ("(rbf 0.5)", 700, 8, 300),
+            ("(rbf 2.5)", 900, 40, 16),
             ("(+ (scale 2.0 (rbf 0.4)) (scale 0.5 (matern32 0.9)))", 2049, 6, 20),
             ("(scale 1.5 (matern32 0.5))", 4096, 8, 16), ("(* (rbf 0.8) (matern52 1.1))", 129, 5, 33)]
 

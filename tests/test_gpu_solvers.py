@@ -163,3 +163,17 @@ def test_evidence_optimizer_matches_reference(gpu_ctx):
     assert cfg.evaluations == int(g["gp_evals"]) == 21
     np.testing.assert_allclose(np.array(trace), g["gp_trace"], rtol=1e-4)
     np.testing.assert_allclose(best, g["gp_best"], atol=2e-3)
+
+
+@pytest.mark.parametrize("d,expr", [(4, "(matern52 0.7)"), (40, "(rbf 2.5)")])
+def test_symmetric_tensor_core_cg_dims(gpu_ctx, monkeypatch, d, expr):
+    """The default CG matvec for r^2 trees (K1-TC-sym) at the smallest and a
+    large feature dimension: same iterations / solution as the SIMT kernel."""
+    x, b = small_inputs(2500, d, 43)
+    k = G.parse_kernel(expr)
+    monkeypatch.setenv("LGP_NO_TCSYM", "1")
+    base = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
+    monkeypatch.delenv("LGP_NO_TCSYM")
+    res = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
+    assert abs(res.iterations - base.iterations) <= max(2, 0.03 * base.iterations)
+    assert rel_l2(res.x, base.x) <= 1e-4
