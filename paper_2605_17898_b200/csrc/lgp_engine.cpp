@@ -232,8 +232,11 @@ void MatvecOp::prepare() {
   // symmetric block-pair kernel for the square operator on a single rank
   // block-pair partials: 2 x rows_per_cta FP64 per unit, n_rb^2 / 2 units
   const double sym_bytes = (double)n_rb * (n_rb + 1) / 2.0 * rows_per_cta * 16.0 * n_pass * tb;
+  // (and enough block pairs to fill the GPU: small operators take the plain
+  // kernel, whose column segments supply the parallelism)
   sym = (rows == cols) && ctx->world == 1 && tb == 1 && !(flags & LGP_NO_SYM) &&
-        (rows_per_cta % tu.cc) == 0 && n_rb >= 2 && sym_bytes <= kSymPartialBudget;
+        (rows_per_cta % tu.cc) == 0 && (int64_t)n_rb * (n_rb + 1) / 2 >= 2 * ctx->sm_count &&
+        sym_bytes <= kSymPartialBudget;
   if (sym) {
     n_cols_pad = n_rows_pad;  // column blocks = row blocks
     n_tiles = n_cols_pad / tu.cc;
