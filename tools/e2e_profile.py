@@ -18,8 +18,8 @@ _lib.check(lib.lgp_host_alloc(x.nbytes, C.byref(hx)))
 _lib.check(lib.lgp_host_alloc(z.nbytes, C.byref(hv)))
 px = np.ctypeslib.as_array(C.cast(hx, C.POINTER(C.c_double)), shape=x.shape); px[...] = x
 pv = np.ctypeslib.as_array(C.cast(hv, C.POINTER(C.c_double)), shape=z.shape); pv[...] = z
-for _ in range(3):
-    G.matrix_free_matvec(k, px, 0.1, pv)
+for _ in range(12):
+    res = G.matrix_free_matvec(k, px, 0.1, pv)
 T = {}
 def tic(name, f):
     t0 = time.perf_counter(); r = f(); T[name] = T.get(name, 0) + time.perf_counter() - t0; return r
@@ -28,8 +28,8 @@ for _ in range(5):
     va = tic("as_block", lambda: G.linalg.as_block(pv))
     prog = tic("program", lambda: G.kernels.program(k))
     pts = tic("points_upload", lambda: _lib.DevicePoints(ctx, xa))
-    out = tic("np.empty", lambda: np.empty(va.shape))
-    tic("lgp_matvec", lambda: _lib.check(lib.lgp_matvec(ctx.handle, prog.handle, pts.handle, pts.handle, 0.1, _lib.vptr(va), 16, _lib.vptr(out), 0)))
+    out = tic("result_buffer", lambda: _lib.result_buffer(va.shape))
+    tic("lgp_matvec", lambda: _lib.check(lib.lgp_matvec(ctx.handle, prog.handle, pts.handle, pts.handle, 0.1, _lib.vptr(va), 16, _lib.vptr(out), _lib.INPUTS_FINITE)))
     tic("points_free", lambda: pts.__del__())
     t0 = time.perf_counter(); G.matrix_free_matvec(k, px, 0.1, pv); T["full_call"] = T.get("full_call", 0) + time.perf_counter() - t0
 for kk, v in T.items():
