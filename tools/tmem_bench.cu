@@ -14,12 +14,12 @@ constexpr int IT = 2048;
 
 // MODE 0: ld 32x32b.x32 (x2 per iter, one wait); 1: st 32x32b.x32 (x2, one wait);
 // 2: ld 16x256b.x8 (x2, one wait); 3: ld + st (epilogue-like)
-template <int MODE>
+template <int MODE, int COLS = 512>
 __global__ void kern(long long* out, unsigned* sink) {
   __shared__ unsigned tslot;
   const int warp = threadIdx.x / 32;
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(saddr(&tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tslot)), "n"(COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -27,7 +27,7 @@ __global__ void kern(long long* out, unsigned* sink) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const unsigned tmem = tslot;
   const unsigned lanes = (unsigned)(32 * (warp & 3)) << 16;
-  const unsigned col = 128u * (unsigned)((warp >> 2) & 3);
+  const unsigned col = COLS == 512 ? 128u * (unsigned)((warp >> 2) & 3) : 64u * (unsigned)((warp >> 2) & 1);
   unsigned v[64];
   for (int i = 0; i < 64; ++i) v[i] = i * threadIdx.x;
   unsigned acc = 0;
@@ -83,7 +83,7 @@ __global__ void kern(long long* out, unsigned* sink) {
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(COLS));
   }
 }
 
@@ -105,6 +105,50 @@ void run(const char* name, int warps) {
   cudaFree(sink);
 }
 
+// two co-resident CTAs per SM, 256 TMEM columns each: is the ld limit per SM or per CTA?
+void run_two(int warps) {
+  long long* d;
+  unsigned* sink;
+  cudaMalloc(&d, 296 * 8);
+  cudaMalloc(&sink, 296 * 1024 * 4);
+  kern<0, 256><<<296, 32 * warps>>>(d, sink);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  const double bytes = (double)IT * warps * 32 * 64 * 4;
+  printf("2 CTAs/SM x %d warps: %.1f B/clk per CTA (x2 per SM if co-resident) %s\n", warps, bytes / h,
+         e ? cudaGetErrorString(e) : "");
+  fflush(stdout);
+}
+
+// same total tcgen05.ld work, 1 CTA/SM x 8 warps vs 2 CTAs/SM x 4 warps: wall time by events
+void run_total() {
+  long long* d;
+  unsigned* sink;
+  cudaMalloc(&d, 296 * 8);
+  cudaMalloc(&sink, 296 * 1024 * 4);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int rep = 0; rep < 2; ++rep) {
+    float ms1, ms2;
+    cudaEventRecord(e0);
+    kern<0, 512><<<148, 256>>>(d, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms1, e0, e1);
+    cudaEventRecord(e0);
+    kern<0, 256><<<296, 128>>>(d, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms2, e0, e1);
+    const double bytes = (double)IT * 8 * 32 * 64 * 4 * 148;
+    printf("1 CTA/SM x 8 warps: %.3f ms (%.1f B/clk/SM at 1965 MHz); 2 CTAs/SM x 4 warps: %.3f ms (%.1f B/clk/SM)\n",
+           ms1, bytes / (ms1 * 1e-3 * 1.965e9) / 148, ms2, bytes / (ms2 * 1e-3 * 1.965e9) / 148);
+  }
+  fflush(stdout);
+}
+
 int main(int argc, char** argv) {
   const int mode = argc > 1 ? atoi(argv[1]) : 0;
   for (int w : {4, 8, 16}) {
@@ -114,6 +158,8 @@ int main(int argc, char** argv) {
     if (mode == 3) run<3>("ld+st 32x32b (64 cols)", w);
     if (mode == 4) run<4>("ld 32x32b.x64 (64 cols)", w);
     if (mode == 5) run<5>("ld x32 x2, wait every 2nd", w);
+    if (mode == 6 && w <= 8) run_two(w);
+    if (mode == 7 && w == 4) run_total();
   }
   return 0;
 }
