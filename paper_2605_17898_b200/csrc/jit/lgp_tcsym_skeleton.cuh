@@ -27,6 +27,9 @@
 #ifndef LGP_TS_NWG
 #define LGP_TS_NWG 4  // epilogue warpgroups (chunks round-robin): latency hiding
 #endif
+#ifndef LGP_TS_LAYOUT
+#define LGP_TS_LAYOUT 1  // 1: 16x256b TMEM tiles (4 rows x 8 columns per thread); 0: 32x32b rows
+#endif
 #define TS_THREADS (64 + 128 * LGP_TS_NWG)
 #ifndef LGP_TS_NSB
 #define LGP_TS_NSB (LGP_TS_NWG == 4 ? 8 : 6)  // S buffers of 64 TMEM columns
@@ -47,6 +50,28 @@
 __device__ __forceinline__ double lgp_widen_nn(float f) {
   const unsigned b = __float_as_uint(f);
   return __hiloint2double((b >> 3) + 0x38000000u, b << 29);
+}
+
+// 16 TMEM lanes x 32 columns: thread t gets, for each 8-column block b,
+// regs 4b, 4b+1 = (lane t/4, columns 8b + 2(t%4), +1) and regs 4b+2, 4b+3 = the
+// same columns of lane t/4 + 8 (profiles/r01_hw_microbench.txt, shape check)
+__device__ __forceinline__ void lgp_tmem_ld16x256_x4(unsigned taddr, unsigned* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : LGP_R8(v, 0), LGP_R8(v, 8)
+      : "r"(taddr));
+}
+
+// transposing FP64 reduction over lane bit o: lanes with the bit clear keep
+// entries [0, h), the others [h, 2h); each half is summed with the partner's
+template <int H>
+__device__ __forceinline__ void lgp_xreduce(double* x, int o, bool up) {
+#pragma unroll
+  for (int m = 0; m < H; ++m) {
+    const double send = up ? x[m] : x[m + H];
+    const double keep = up ? x[m + H] : x[m];
+    x[m] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+  }
 }
 
 extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(const LgpTcSymArgs a) {
@@ -139,6 +164,116 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
     __syncwarp();
   } else {
     // -------------------------------------------------- epilogue warpgroups
+#if LGP_TS_LAYOUT == 1
+    // Each warp reads its 32 TMEM lanes as two 16x256b tiles per 32 columns:
+    // thread t holds rows r0 + {0, 8, 16, 24} (r0 = t/4) x 8 columns
+    // {8b + 2(t%4) + e}. The row side keeps 4 FP64 accumulators (reduced over
+    // the 4 lanes of a row once per work item); the column side first sums its
+    // 4 rows in registers, then a 3-level transposing butterfly over the 8
+    // lanes sharing t%4 leaves one column per lane.
+    const int w = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r0 = lane >> 2, cq = lane & 3;
+    const int nloc = (nch - w + LGP_TS_NWG - 1) / LGP_TS_NWG;
+    lgp_mbar_wait(TBAR(TSB_AFULL), 0);
+    double vi[4], acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // u = 2h + v: row 32 q4 + 16 h + 8 v + r0
+      vi[u] = vis[32 * q4 + 16 * (u >> 1) + 8 * (u & 1) + r0];
+      acc[u] = 0.0;
+    }
+    // after the butterfly lane t holds column 8 k + 2 cq + e, k = 2 b4 + b3, e = b2
+    const int ccol = 8 * (2 * ((lane >> 4) & 1) + ((lane >> 3) & 1)) + 2 * cq + ((lane >> 2) & 1);
+    for (int k = 0; k < nloc; ++k) {
+      const int c = LGP_TS_NWG * k + w;
+      const int q = w + LGP_TS_NWG * (k % TS_NSBW);
+      const int s = c % LGP_TC_STAGES;
+      const int chunk = c0 + c;
+      lgp_mbar_wait(TBAR(TSB_S1FULL(q)), (k / TS_NSBW) & 1);
+      lgp_tc_fence_after();
+      lgp_mbar_wait(TBAR(TSB_SFULL(s)), (c / LGP_TC_STAGES) & 1);  // p chunk visible
+      const double* vj = reinterpret_cast<const double*>(stg + (size_t)s * TS_STAGE_BYTES + TC_B1_BYTES);
+      const bool diag = chunk < 2 * I + 2;
+      // diagonal chunks: column offset relative to this thread's first row
+      const int dj0 = chunk * TC_CH - (128 * I + 32 * q4 + r0) + 2 * cq;
+      double* cb = cbuf + ((size_t)(w * 2 + (k & 1)) * 4 + q4) * TC_CH;
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        unsigned sv[2][16];
+        lgp_tmem_ld16x256_x4(TS_SB(q) + ((unsigned)(32 * q4) << 16) + 32u * g, sv[0]);
+        lgp_tmem_ld16x256_x4(TS_SB(q) + ((unsigned)(32 * q4 + 16) << 16) + 32u * g, sv[1]);
+        lgp_tmem_wait_ld();
+        if (g == 1) {
+          lgp_tc_fence_before();
+          __syncwarp();
+          if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SFREE(q)));  // S buffer free for the next GEMM
+        }
+        double pj[8];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double2 t2 = *reinterpret_cast<const double2*>(vj + 32 * g + 8 * b + 2 * cq);
+          pj[2 * b] = t2.x;
+          pj[2 * b + 1] = t2.y;
+        }
+        double cv[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) cv[m] = 0.0;
+        // two separate unrolled loops: a per-entry diag test would cost a
+        // branch + convergence barrier per entry (ncu: BSSY/BSYNC 17 % of issue)
+        if (!diag) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+              const int u = 2 * h + ((r >> 1) & 1), m = 2 * (r >> 2) + (r & 1);
+              const double kd = lgp_widen_nn(lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[h][r])), a, 0));
+              acc[u] = fma(kd, pj[m], acc[u]);
+              cv[m] = fma(kd, vi[u], cv[m]);
+            }
+        } else {
+          // diagonal block: row side j >= i, column side j > i
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+              const int b = r >> 2, e = r & 1;
+              const int u = 2 * h + ((r >> 1) & 1), m = 2 * b + e;
+              const float kk = lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[h][r])), a, 0);
+              const int dj = dj0 + 32 * g + 8 * b + e - (16 * h + 8 * ((r >> 1) & 1));  // j - i
+              acc[u] = fma(lgp_widen_nn(dj >= 0 ? kk : 0.f), pj[m], acc[u]);
+              cv[m] = fma(lgp_widen_nn(dj > 0 ? kk : 0.f), vi[u], cv[m]);
+            }
+        }
+        lgp_xreduce<4>(cv, 16, (lane & 16) != 0);
+        lgp_xreduce<2>(cv, 8, (lane & 8) != 0);
+        lgp_xreduce<1>(cv, 4, (lane & 4) != 0);
+        cb[32 * g + ccol] = cv[0];
+      }
+      __syncwarp();
+      if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SEMPTY(s)));  // p chunk read: stage reusable
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + w) : "memory");
+      // column partials of this (I, chunk): warps 0..3 in a fixed order
+      if (lane < 16) {
+        const int j = 16 * q4 + lane;
+        const double* b0 = cbuf + (size_t)(w * 2 + (k & 1)) * 4 * TC_CH;
+        const double sum = ((b0[j] + b0[TC_CH + j]) + b0[2 * TC_CH + j]) + b0[3 * TC_CH + j];
+        a.colpart[(size_t)(a.colbase[I] + chunk - 2 * I) * TC_CH + j] = sum;
+      }
+    }
+    // row side: the 4 lanes of a row (lane bits 0, 1) -> lane holds u = 2 b1 + b0
+    lgp_xreduce<2>(acc, 2, (lane & 2) != 0);
+    lgp_xreduce<1>(acc, 1, (lane & 1) != 0);
+    const int ur = 2 * ((lane >> 1) & 1) + (lane & 1);
+    const int row = 32 * q4 + 16 * (ur >> 1) + 8 * (ur & 1) + r0;
+    if (w > 0) comb[(w - 1) * 128 + row] = acc[0];
+    asm volatile("bar.sync %0, %1;" ::"r"(LGP_TS_NWG + 1), "r"(128 * LGP_TS_NWG) : "memory");
+    if (w == 0) {
+      double r = acc[0];
+#pragma unroll
+      for (int u = 1; u < LGP_TS_NWG; ++u) r += comb[(u - 1) * 128 + row];
+      a.rowpart[(size_t)item * 128 + row] = r;
+    }
+#else
     const int w = (warp - 2) >> 2;
     const int q4 = warp & 3;
     const int row = 32 * q4 + lane;
@@ -227,6 +362,7 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
       for (int u = 1; u < LGP_TS_NWG; ++u) r += comb[(u - 1) * 128 + row];
       a.rowpart[(size_t)item * 128 + row] = r;
     }
+#endif
   }
   lgp_tc_fence_before();
   __syncthreads();

