@@ -30,6 +30,9 @@
 #ifndef LGP_TS_LAYOUT
 #define LGP_TS_LAYOUT 1  // 1: 16x256b TMEM tiles (4 rows x 8 columns per thread); 0: 32x32b rows
 #endif
+#ifndef LGP_TS_POLY
+#define LGP_TS_POLY 0  // entries per 16 whose exp2 runs on the FMA pipe (layout 1)
+#endif
 #define TS_THREADS (64 + 128 * LGP_TS_NWG)
 #ifndef LGP_TS_NSB
 #define LGP_TS_NSB (LGP_TS_NWG == 4 ? 8 : 6)  // S buffers of 64 TMEM columns
@@ -47,9 +50,16 @@
 
 // FP32 -> FP64 for finite non-negative kernel values without the conversion
 // pipe: exponent re-bias + mantissa shift (0 maps to 2^-127, negligible)
+#ifndef LGP_TS_WIDEN
+#define LGP_TS_WIDEN 0  // 1: F2F.F64.F32 conversion instead of the integer re-bias
+#endif
 __device__ __forceinline__ double lgp_widen_nn(float f) {
+#if LGP_TS_WIDEN
+  return (double)f;
+#else
   const unsigned b = __float_as_uint(f);
   return __hiloint2double((b >> 3) + 0x38000000u, b << 29);
+#endif
 }
 
 // 16 TMEM lanes x 32 columns: thread t gets, for each 8-column block b,
@@ -226,7 +236,7 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
               const int u = 2 * h + ((r >> 1) & 1), m = 2 * (r >> 2) + (r & 1);
-              const double kd = lgp_widen_nn(lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[h][r])), a, 0));
+              const double kd = lgp_widen_nn(lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[h][r])), a, r < LGP_TS_POLY ? 1 : 0));
               acc[u] = fma(kd, pj[m], acc[u]);
               cv[m] = fma(kd, vi[u], cv[m]);
             }
