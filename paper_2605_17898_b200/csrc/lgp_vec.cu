@@ -47,6 +47,37 @@ __device__ __forceinline__ void block_colsum(double v, int t, double* part_row, 
   __syncthreads();
 }
 
+// Fixed-order (deterministic) column sums of part[nblk][t] by one block, for
+// t <= blockDim.x / 2: thread (g, c) sums rows g, g + G, ... (G = power-of-two
+// floor of blockDim.x / t), then a pairwise tree over g in shared memory.
+// Afterwards sm[c] (c < t) holds column c's sum. All threads must call it.
+// (A single thread per column walking all nblk rows was a ~400-long serial
+// load + DADD chain: 18-25 us per CG / Lanczos scalar step at N = 100k.)
+__device__ __forceinline__ bool part_par(int t) { return 2 * t <= 256; }
+__device__ void part_colsums(const double* __restrict__ part, int nblk, int t, double* sm) {
+  const int G = 1 << (31 - __clz((int)blockDim.x / t));
+  const int tid = threadIdx.x, g = tid / t, c = tid - g * t;
+  if (g < G) {
+    double v = 0.0;
+    for (int b = g; b < nblk; b += G) v += part[(size_t)b * t + c];
+    sm[tid] = v;
+  }
+  __syncthreads();
+  for (int h = G >> 1; h >= 1; h >>= 1) {
+    if (g < h) sm[tid] += sm[tid + h * t];
+    __syncthreads();
+  }
+}
+
+// column c's sum: from sm after part_colsums when part_par(t), else serially
+__device__ __forceinline__ double part_sum(const double* __restrict__ part, int nblk, int t, int c,
+                                           const double* sm) {
+  if (part_par(t)) return sm[c];
+  double v = 0.0;
+  for (int b = 0; b < nblk; ++b) v += part[(size_t)b * t + c];
+  return v;
+}
+
 __global__ void k_dot_partial(const double* __restrict__ a, const double* __restrict__ b,
                               long long n, int t, long long chunk, double* part, const int* done) {
   __shared__ double sm[256];
@@ -64,12 +95,10 @@ __global__ void k_dot_partial(const double* __restrict__ a, const double* __rest
 }
 
 __global__ void k_dot_final(const double* part, int nblk, int t, double* out, const int* done) {
+  __shared__ double sm[256];
   if (is_done(done)) return;
-  for (int c = threadIdx.x; c < t; c += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[(size_t)b * t + c];
-    out[c] = s;
-  }
+  if (part_par(t)) part_colsums(part, nblk, t, sm);
+  for (int c = threadIdx.x; c < t; c += blockDim.x) out[c] = part_sum(part, nblk, t, c, sm);
 }
 
 __global__ void k_pack(const double* __restrict__ V, long long n, int t, long long n_pad, int tb,
@@ -257,10 +286,11 @@ __global__ void k_cg_init_scalars(const double* bb, int t, double rel_tol, CgSta
 }
 
 __global__ void k_cg_fin_pap(const double* part, int nblk, int t, CgState s) {
+  __shared__ double sm[256];
   if (*s.done) return;
+  if (part_par(t)) part_colsums(part, nblk, t, sm);
   for (int c = threadIdx.x; c < t; c += blockDim.x) {
-    double pap = 0.0;
-    for (int b = 0; b < nblk; ++b) pap += part[(size_t)b * t + c];
+    const double pap = part_sum(part, nblk, t, c, sm);
     if (s.active[c]) {
       if (pap <= 0.0) {  // breakdown: operator not SPD (solvers.py:110-113)
         *s.status = 1;
@@ -303,13 +333,14 @@ __global__ void k_cg_update_xr(double* __restrict__ x, double* __restrict__ r,
 
 __global__ void k_cg_fin_rs(const double* part, int nblk, int t, int it, int max_iter,
                             CgState s) {
+  __shared__ double sm[256];
   if (*s.done) return;
   __shared__ int any;
   if (threadIdx.x == 0) any = 0;
+  if (part_par(t)) part_colsums(part, nblk, t, sm);
   __syncthreads();
   for (int c = threadIdx.x; c < t; c += blockDim.x) {
-    double rs_new = 0.0;
-    for (int b = 0; b < nblk; ++b) rs_new += part[(size_t)b * t + c];
+    const double rs_new = part_sum(part, nblk, t, c, sm);
     if (!s.active[c]) continue;
     const double nrm = sqrt(rs_new);
     if (nrm <= s.tol[c] || it >= max_iter) {  // converged, or budget spent (reported)
@@ -355,10 +386,11 @@ __global__ void k_lz_init_scalars(const double* zz, int t, LzState s) {
 }
 
 __global__ void k_lz_fin_alpha(const double* part, int nblk, int t, int j, int steps, LzState s) {
+  __shared__ double sm[256];
   if (*s.done) return;
+  if (part_par(t)) part_colsums(part, nblk, t, sm);
   for (int c = threadIdx.x; c < t; c += blockDim.x) {
-    double a = 0.0;
-    for (int b = 0; b < nblk; ++b) a += part[(size_t)b * t + c];
+    const double a = part_sum(part, nblk, t, c, sm);
     if (s.active[c]) {
       s.alpha[(size_t)c * steps + j] = a;
       s.a_cur[c] = a;
@@ -385,41 +417,86 @@ __global__ void k_lz_update1(double* __restrict__ w, const double* __restrict__ 
 }
 
 // part[blk][k][c] = sum over this block's rows of basis[k][i][c] * w[i][c], k < nb
+constexpr int kLzBatch = 8;
 __global__ void k_lz_multidot(const double* __restrict__ basis, long long stride_k, int nb,
                               const double* __restrict__ w, long long n, int t, long long chunk,
                               double* part, const int* done) {
-  __shared__ double sm[256];
+  __shared__ double sm[kLzBatch * 256];
   if (is_done(done)) return;
   const int tid = threadIdx.x;
+  const int bd = blockDim.x;  // = t * (256 / t): every thread owns a column
   const int c = tid % t;
-  const int stride = blockDim.x / t;
+  const int stride = bd / t;
   const long long r0 = (long long)blockIdx.x * chunk;
   long long r1 = r0 + chunk;
   if (r1 > n) r1 = n;
-  // basis vectors in batches of 4: w is read once per batch and the four
-  // independent FMA chains keep more loads in flight (per-(k, c) summation
-  // order is unchanged: rows in stride order)
-  for (int k0 = 0; k0 < nb; k0 += 4) {
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
-    if (tid < stride * t)
-      for (long long i = r0 + tid / t; i < r1; i += stride) {
-        const long long e = i * t + c;
-        const double wv = w[e];
+  // basis vectors in batches of 8: w is read once per batch, 8 independent
+  // FMA chains keep loads in flight, and one shared-memory pass reduces the
+  // batch (per-(k, c) summation order: rows in stride order, then the block's
+  // threads of column c in tid order, as block_colsum)
+  for (int k0 = 0; k0 < nb; k0 += kLzBatch) {
+    double s[kLzBatch];
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          if (k0 + kk < nb) s[kk] = fma(basis[(size_t)(k0 + kk) * stride_k + e], wv, s[kk]);
+    for (int kk = 0; kk < kLzBatch; ++kk) s[kk] = 0.0;
+    // 4 rows per iteration: all 4 x (1 + 8) loads issue before the FMAs
+    // (one memory latency per 4 rows instead of per row)
+    long long i = r0 + tid / t;
+    for (; i + 3 * stride < r1; i += 4 * stride) {
+      double wv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) wv[u] = w[(i + u * stride) * t + c];
+#pragma unroll
+      for (int kk = 0; kk < kLzBatch; ++kk)
+        if (k0 + kk < nb) {
+          const double* bk = basis + (size_t)(k0 + kk) * stride_k + c;
+          double bv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) bv[u] = bk[(i + u * stride) * t];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s[kk] = fma(bv[u], wv[u], s[kk]);
+        }
+    }
+    for (; i < r1; i += stride) {
+      const long long e = i * t + c;
+      const double wv = w[e];
+#pragma unroll
+      for (int kk = 0; kk < kLzBatch; ++kk)
+        if (k0 + kk < nb) s[kk] = fma(basis[(size_t)(k0 + kk) * stride_k + e], wv, s[kk]);
+    }
+#pragma unroll
+    for (int kk = 0; kk < kLzBatch; ++kk) sm[kk * 256 + tid] = s[kk];
+    __syncthreads();
+    for (int o = tid; o < kLzBatch * t; o += bd) {
+      const int kk = o / t, cc = o - kk * t;
+      if (k0 + kk < nb) {
+        double r = 0.0;
+        for (int q = cc; q < bd; q += t) r += sm[kk * 256 + q];
+        part[((size_t)blockIdx.x * nb + k0 + kk) * t + cc] = r;
       }
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-      if (k0 + kk < nb) block_colsum(s[kk], t, part + ((size_t)blockIdx.x * nb + k0 + kk) * t, sm);
+    }
+    __syncthreads();
   }
 }
 
-__global__ void k_lz_fin_h(const double* part, int nblk, int nb, int t, LzState s) {
+// h[e] = sum over blocks of part[blk][e], e < m = nb * t: 32 entries per block
+// (coalesced rows), 8 warps over the blocks (b = warp, warp + 8, ...), combined
+// in warp order (deterministic)
+__global__ void __launch_bounds__(256) k_lz_fin_h(const double* part, int nblk, int nb, int t,
+                                                  LzState s) {
+  __shared__ double sm[8][32];
   if (*s.done) return;
-  for (int e = threadIdx.x; e < nb * t; e += blockDim.x) {
+  const int m = nb * t;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  double v = 0.0;
+  if (e < m)
+    for (int b = wp; b < nblk; b += 8) v += part[(size_t)b * m + e];
+  sm[wp][lane] = v;
+  __syncthreads();
+  if (wp == 0 && e < m) {
     double h = 0.0;
-    for (int b = 0; b < nblk; ++b) h += part[(size_t)b * nb * t + e];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) h += sm[u][lane];
     s.h[e] = h;
   }
 }
@@ -444,12 +521,57 @@ __global__ void k_lz_update2(double* __restrict__ w, const double* __restrict__ 
   double acc = 0.0;
   if (tid < stride * t) {
     const bool act = s.active[c] != 0;
-    for (long long i = r0 + tid / t; i < r1; i += stride) {
+    // two rows per iteration, 8 independent chains over k each (16 loads in
+    // flight), summed pairwise; per-row arithmetic identical for both loops
+    long long i = r0 + tid / t;
+    for (; i + stride < r1; i += 2 * stride) {
+      const long long e0 = i * t + c, e1 = e0 + (long long)stride * t;
+      double v0 = w[e0], v1 = w[e1];
+      if (act) {
+        double a8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        double b8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        int k = 0;
+        for (; k + 8 <= nb; k += 8) {
+          double x0[8], x1[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            x0[kk] = basis[(size_t)(k + kk) * stride_k + e0];
+            x1[kk] = basis[(size_t)(k + kk) * stride_k + e1];
+          }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const double hk = h[(k + kk) * t + c];
+            a8[kk] = fma(x0[kk], hk, a8[kk]);
+            b8[kk] = fma(x1[kk], hk, b8[kk]);
+          }
+        }
+        for (; k < nb; ++k) {
+          const double hk = h[k * t + c];
+          a8[0] = fma(basis[(size_t)k * stride_k + e0], hk, a8[0]);
+          b8[0] = fma(basis[(size_t)k * stride_k + e1], hk, b8[0]);
+        }
+        const double u0 = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+        const double u1 = ((b8[0] + b8[1]) + (b8[2] + b8[3])) + ((b8[4] + b8[5]) + (b8[6] + b8[7]));
+        v0 = __dsub_rn(v0, u0);
+        v1 = __dsub_rn(v1, u1);
+        w[e0] = v0;
+        w[e1] = v1;
+      }
+      acc = fma(v0, v0, acc);
+      acc = fma(v1, v1, acc);
+    }
+    for (; i < r1; i += stride) {
       const long long e = i * t + c;
       double v = w[e];
       if (act) {
-        double u = 0.0;
-        for (int k = 0; k < nb; ++k) u = fma(basis[(size_t)k * stride_k + e], h[k * t + c], u);
+        double u8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        int k = 0;
+        for (; k + 8 <= nb; k += 8)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            u8[kk] = fma(basis[(size_t)(k + kk) * stride_k + e], h[(k + kk) * t + c], u8[kk]);
+        for (; k < nb; ++k) u8[0] = fma(basis[(size_t)k * stride_k + e], h[k * t + c], u8[0]);
+        const double u = ((u8[0] + u8[1]) + (u8[2] + u8[3])) + ((u8[4] + u8[5]) + (u8[6] + u8[7]));
         v = __dsub_rn(v, u);
         w[e] = v;
       }
@@ -460,13 +582,14 @@ __global__ void k_lz_update2(double* __restrict__ w, const double* __restrict__ 
 }
 
 __global__ void k_lz_fin_beta(const double* part, int nblk, int t, int j, int steps, LzState s) {
+  __shared__ double sm[256];
   if (*s.done) return;
   __shared__ int any;
   if (threadIdx.x == 0) any = 0;
+  if (part_par(t)) part_colsums(part, nblk, t, sm);
   __syncthreads();
   for (int c = threadIdx.x; c < t; c += blockDim.x) {
-    double ss = 0.0;
-    for (int b = 0; b < nblk; ++b) ss += part[(size_t)b * t + c];
+    const double ss = part_sum(part, nblk, t, c, sm);
     if (!s.active[c]) continue;
     const double nb = sqrt(ss);
     const double a = fabs(s.a_cur[c]);
@@ -553,23 +676,47 @@ __global__ void k_pt_radius(const double* __restrict__ x, long long n, int d,
   if ((threadIdx.x & 31) == 0 && isfinite(m)) atomicMax(r2max, __double_as_longlong(m));
 }
 
-__global__ void k_tcsym_epilogue(const double* __restrict__ rowpart,
-                                 const double* __restrict__ colpart, const int* __restrict__ item0,
-                                 const int* __restrict__ nseg, const long long* __restrict__ colbase,
-                                 long long n, double scale, double noise,
-                                 const double* __restrict__ noise_v, double* __restrict__ out,
-                                 const int* done) {
+// One block per 64-column chunk c: out[64c + jj] = scale * (row partials of
+// that row over its segments + column partials of chunk c over the row blocks
+// I2 <= c / 2) + noise * v. The column sum (up to N / 128 terms) is split over
+// kTsGroups thread groups (I2 = g, g + G, ...) and combined in g order: fixed
+// order, deterministic. (One thread per output walking all I2 serially was
+// latency-bound: 125 us at cfg4 for 259 MB of partials.)
+constexpr int kTsGroups = 8;
+__global__ void __launch_bounds__(64 * kTsGroups)
+    k_tcsym_epilogue(const double* __restrict__ rowpart, const double* __restrict__ colpart,
+                     const int* __restrict__ item0, const int* __restrict__ nseg,
+                     const long long* __restrict__ colbase, long long n, double scale,
+                     double noise, const double* __restrict__ noise_v, double* __restrict__ out,
+                     const int* done) {
+  __shared__ double part[kTsGroups][64];
   if (is_done(done)) return;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int I = (int)(i >> 7), r = (int)(i & 127);
-    const long long c = i >> 6;
-    const int jj = (int)(i & 63);
-    double s = 0.0;
+  const long long c = blockIdx.x;
+  const int jj = threadIdx.x & 63, g = threadIdx.x >> 6;
+  const long long last = c >> 1;
+  double s = 0.0;
+  long long I2 = g;
+  for (; I2 + 3 * kTsGroups <= last; I2 += 4 * kTsGroups) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long J = I2 + u * kTsGroups;
+      v[u] = colpart[(size_t)(colbase[J] + c - 2 * J) * 64 + jj];
+    }
+    s = (((s + v[0]) + v[1]) + v[2]) + v[3];
+  }
+  for (; I2 <= last; I2 += kTsGroups) s += colpart[(size_t)(colbase[I2] + c - 2 * I2) * 64 + jj];
+  part[g][jj] = s;
+  __syncthreads();
+  const long long i = c * 64 + jj;
+  if (g == 0 && i < n) {
+    const int I = (int)(c >> 1), r = (int)((c & 1) * 64 + jj);
     const int f = item0[I], m = nseg[I];
-    for (int k = 0; k < m; ++k) s += rowpart[(size_t)(f + k) * 128 + r];
-    for (long long I2 = 0; 2 * I2 <= c; ++I2) s += colpart[(size_t)(colbase[I2] + c - 2 * I2) * 64 + jj];
-    double o = __dmul_rn(scale, s);
+    double t = 0.0;
+    for (int k = 0; k < m; ++k) t += rowpart[(size_t)(f + k) * 128 + r];
+#pragma unroll
+    for (int u = 0; u < kTsGroups; ++u) t += part[u][jj];
+    double o = __dmul_rn(scale, t);
     if (noise_v != nullptr && noise != 0.0) o = __dadd_rn(o, __dmul_rn(noise, noise_v[i]));
     out[i] = o;
   }
@@ -630,8 +777,9 @@ void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int
 void tcsym_epilogue(Context* c, const double* rowpart, const double* colpart, const int* item0,
                     const int* nseg, const long long* colbase, int64_t n, double scale,
                     double noise, const double* noise_v, double* out, const int* done) {
-  k_tcsym_epilogue<<<grid_for(n), 256, 0, c->stream>>>(rowpart, colpart, item0, nseg, colbase, n,
-                                                       scale, noise, noise_v, out, done);
+  if (n <= 0) return;
+  k_tcsym_epilogue<<<(unsigned)((n + 63) / 64), 64 * kTsGroups, 0, c->stream>>>(
+      rowpart, colpart, item0, nseg, colbase, n, scale, noise, noise_v, out, done);
   LGP_LAUNCH_CHECK(c);
 }
 
@@ -746,7 +894,7 @@ void lz_multidot(Context* c, const double* basis, int64_t stride, int nb, const 
 }
 
 void lz_fin_h(Context* c, const double* part, int nblk, int nb, int t, LzState s) {
-  k_lz_fin_h<<<1, 256, 0, c->stream>>>(part, nblk, nb, t, s);
+  k_lz_fin_h<<<(nb * t + 31) / 32, 256, 0, c->stream>>>(part, nblk, nb, t, s);
   LGP_LAUNCH_CHECK(c);
 }
 

@@ -18,6 +18,8 @@ Public names and argument conventions follow the reference:
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from typing import NamedTuple
 
@@ -188,10 +190,28 @@ def probe_block(n, count, seed):
     one PCG64 child stream per probe, so the first k of `count` probes do not
     depend on `count`."""
     z = np.empty((n, count))
-    for c, child in enumerate(np.random.SeedSequence(seed).spawn(count)):
-        rng = np.random.Generator(np.random.PCG64(child))
+    kids = np.random.SeedSequence(seed).spawn(count)
+
+    def draw(c):
+        rng = np.random.Generator(np.random.PCG64(kids[c]))
         z[:, c] = rng.integers(0, 2, size=n) * 2.0 - 1.0
+
+    if n * count < (1 << 18) or count == 1:
+        for c in range(count):
+            draw(c)
+    else:  # independent streams; the ufunc / strided column writes release the GIL
+        list(_probe_pool().map(draw, range(count)))
     return z
+
+
+_POOL = None
+
+
+def _probe_pool():
+    global _POOL
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1)))
+    return _POOL
 
 
 def gauss_quadrature(alphas, betas):
