@@ -30,8 +30,22 @@
 #ifndef LGP_TS_LAYOUT
 #define LGP_TS_LAYOUT 1  // 1: 16x256b TMEM tiles (4 rows x 8 columns per thread); 0: 32x32b rows
 #endif
+#ifndef LGP_TS_PF
+#define LGP_TS_PF 0  // 1: issue the second 32-column half's TMEM loads before the first half's math
+#endif
+#ifndef LGP_TS_ABLATE
+#define LGP_TS_ABLATE 0
+#endif
 #ifndef LGP_TS_POLY
 #define LGP_TS_POLY 0  // entries per 16 whose exp2 runs on the FMA pipe (layout 1)
+#endif
+#ifndef LGP_TS_XPOSE
+#define LGP_TS_XPOSE 0  // 1: column reduction through a swizzled shared-memory transpose (slower: 2.39 vs 2.30 ms); 0: butterfly
+#endif
+#if LGP_TS_XPOSE && LGP_TS_LAYOUT == 1
+#define TS_XPOSE_DOUBLES (LGP_TS_NWG * 4 * 32 * 8)
+#else
+#define TS_XPOSE_DOUBLES 0
 #endif
 #define TS_THREADS (64 + 128 * LGP_TS_NWG)
 #ifndef LGP_TS_NSB
@@ -96,7 +110,8 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
   unsigned char* stg = ts_smem + TC_A1_BYTES + 128 * 8;
   double* cbuf = reinterpret_cast<double*>(stg + LGP_TC_STAGES * TS_STAGE_BYTES);
   double* comb = cbuf + TS_CBUF_BYTES / 8;  // [NWG - 1][128] row sums of warpgroups 1..
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(comb + 128 * (LGP_TS_NWG - 1));
+  double* xpose = comb + 128 * (LGP_TS_NWG - 1);  // [epilogue warp][32 lanes][8] column transposes
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(xpose + TS_XPOSE_DOUBLES);
   unsigned* tslot = reinterpret_cast<unsigned*>(bars + TS_NBARS);
   const unsigned bar0 = lgp_saddr(bars);
 #define TBAR(i) (bar0 + 8u * (unsigned)(i))
@@ -207,8 +222,27 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
       // diagonal chunks: column offset relative to this thread's first row
       const int dj0 = chunk * TC_CH - (128 * I + 32 * q4 + r0) + 2 * cq;
       double* cb = cbuf + ((size_t)(w * 2 + (k & 1)) * 4 + q4) * TC_CH;
+#if LGP_TS_PF
+      // both 32-column halves in flight: the second half's TMEM latency hides
+      // behind the first half's arithmetic
+      unsigned svv[2][2][16];
+      lgp_tmem_ld16x256_x4(TS_SB(q) + ((unsigned)(32 * q4) << 16), svv[0][0]);
+      lgp_tmem_ld16x256_x4(TS_SB(q) + ((unsigned)(32 * q4 + 16) << 16), svv[0][1]);
+      lgp_tmem_wait_ld();
+      lgp_tmem_ld16x256_x4(TS_SB(q) + ((unsigned)(32 * q4) << 16) + 32u, svv[1][0]);
+      lgp_tmem_ld16x256_x4(TS_SB(q) + ((unsigned)(32 * q4 + 16) << 16) + 32u, svv[1][1]);
+#endif
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
+#if LGP_TS_PF
+        unsigned (&sv)[2][16] = svv[g];
+        if (g == 1) {
+          lgp_tmem_wait_ld();
+          lgp_tc_fence_before();
+          __syncwarp();
+          if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SFREE(q)));  // S buffer free for the next GEMM
+        }
+#else
         unsigned sv[2][16];
         lgp_tmem_ld16x256_x4(TS_SB(q) + ((unsigned)(32 * q4) << 16) + 32u * g, sv[0]);
         lgp_tmem_ld16x256_x4(TS_SB(q) + ((unsigned)(32 * q4 + 16) << 16) + 32u * g, sv[1]);
@@ -218,6 +252,7 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
           __syncwarp();
           if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SFREE(q)));  // S buffer free for the next GEMM
         }
+#endif
         double pj[8];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -236,7 +271,11 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
               const int u = 2 * h + ((r >> 1) & 1), m = 2 * (r >> 2) + (r & 1);
+#if (LGP_TS_ABLATE & 2)
+              const double kd = lgp_widen_nn(__uint_as_float(sv[h][r]) * 0.5f);
+#else
               const double kd = lgp_widen_nn(lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[h][r])), a, r < LGP_TS_POLY ? 1 : 0));
+#endif
               acc[u] = fma(kd, pj[m], acc[u]);
               cv[m] = fma(kd, vi[u], cv[m]);
             }
@@ -254,14 +293,43 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
               cv[m] = fma(lgp_widen_nn(dj > 0 ? kk : 0.f), vi[u], cv[m]);
             }
         }
+#if (LGP_TS_ABLATE & 1)  // timing diagnostics only (wrong results)
+        cb[32 * g + ccol] = ((cv[0] + cv[1]) + (cv[2] + cv[3])) + ((cv[4] + cv[5]) + (cv[6] + cv[7]));
+#elif LGP_TS_XPOSE
+        {
+          // lane t stores its 8 column partials as 4 x 16 B (pair position
+          // swizzled by (t >> 1) & 3: conflict-free), then lane l sums slot
+          // l >> 2 of the 8 lanes sharing its column group, rows in order
+          // (4 STS.128 + 8 LDS.64 + 7 DADD per 32 entries; the butterfly
+          // needed 14 SHFL + 28 FSEL + 7 DADD)
+          double* xw = xpose + (size_t)(warp - 2) * 32 * 8;
+          const int sw = (lane >> 1) & 3;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<double2*>(xw + lane * 8 + 2 * (i ^ sw)) = make_double2(cv[2 * i], cv[2 * i + 1]);
+          __syncwarp();
+          const int mm = lane >> 2;
+          double col = 0.0;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const int tt = 4 * r + cq;
+            col += xw[tt * 8 + 2 * ((mm >> 1) ^ ((tt >> 1) & 3)) + (mm & 1)];
+          }
+          __syncwarp();  // the next half overwrites xw
+          cb[32 * g + ccol] = col;
+        }
+#else
         lgp_xreduce<4>(cv, 16, (lane & 16) != 0);
         lgp_xreduce<2>(cv, 8, (lane & 8) != 0);
         lgp_xreduce<1>(cv, 4, (lane & 4) != 0);
         cb[32 * g + ccol] = cv[0];
+#endif
       }
       __syncwarp();
       if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SEMPTY(s)));  // p chunk read: stage reusable
+#if !(LGP_TS_ABLATE & 4)
       asm volatile("bar.sync %0, 128;" ::"r"(1 + w) : "memory");
+#endif
       // column partials of this (I, chunk): warps 0..3 in a fixed order
       if (lane < 16) {
         const int j = 16 * q4 + lane;

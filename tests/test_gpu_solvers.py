@@ -127,13 +127,15 @@ def test_model_small_matrix_free_branch(gpu_ctx, name):
     assert abs(lml - float(g[f"{name}_lml"])) <= 1e-4 * abs(float(g[f"{name}_lml"]))
 
 
-@pytest.mark.parametrize("nwg,layout", [("4", "1"), ("3", "1"), ("2", "1"), ("4", "0")])
-def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg, layout):
+@pytest.mark.parametrize("nwg,layout,xpose", [("4", "1", "1"), ("3", "1", "1"), ("2", "1", "1"),
+                                               ("4", "1", "0"), ("4", "0", "0")])
+def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg, layout, xpose):
     """The symmetric tensor-core CG matvec (default for D >= 4 r^2 trees)
     evaluates each unordered pair once: exactly symmetric, so CG matches the
     symmetric SIMT kernel's (LGP_NO_TCSYM) iteration count and solution, and
     the matvec meets the 1e-5 bar, for every epilogue warpgroup count and
-    both TMEM read layouts (1: 16x256b tiles, 0: 32x32b rows)."""
+    both TMEM read layouts (1: 16x256b tiles, 0: 32x32b rows) and both column
+    reductions (shared-memory transpose, butterfly)."""
     x, b = small_inputs(3000, 8, 41)
     k = G.parse_kernel("(scale 1.2 (rbf 0.6))")
     monkeypatch.setenv("LGP_NO_TCSYM", "1")
@@ -141,6 +143,7 @@ def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg, layout):
     monkeypatch.delenv("LGP_NO_TCSYM")
     monkeypatch.setenv("LGP_TS_NWG", nwg)
     monkeypatch.setenv("LGP_TS_LAYOUT", layout)
+    monkeypatch.setenv("LGP_TS_XPOSE", xpose)
     op = G.KernelOperator(k, x, 0.1)
     res = G.cg_solve(op, b, G.CgConfig(rel_tolerance=1e-8))
     # rounding-order differences move the count either way (215 vs 222 seen
