@@ -92,7 +92,9 @@ int lgp_partition(int64_t n, int world, int rank, int64_t* r0, int64_t* r1);
 /* NCCL unique id (128 bytes) for a multi-rank context; call on rank 0 and
  * broadcast the bytes to the other ranks out of band. */
 int lgp_comm_unique_id(uint8_t* out128);
-/* world == 1: nccl_id may be NULL. */
+/* world == 1: nccl_id may be NULL (no communicator). A non-NULL id at world 1
+ * opens a one-rank NCCL communicator and runs the row-sharded schedule
+ * (device coverage of the multi-GPU path on one GPU). */
 int lgp_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, lgp_ctx** out);
 int lgp_ctx_destroy(lgp_ctx* ctx);
 int lgp_ctx_sync(lgp_ctx* ctx);

@@ -153,7 +153,7 @@ int lgp_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, lgp_
   LGP_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   LGP_CUDA_CHECK(cudaEventCreate(&c->ev0));
   LGP_CUDA_CHECK(cudaEventCreate(&c->ev1));
-  if (world > 1) c->comm = comm_create(rank, world, nccl_id, c->stream);
+  if (world > 1 || nccl_id != nullptr) c->comm = comm_create(rank, world, nccl_id, c->stream);
   {
     std::lock_guard<std::mutex> g(g_ctx_mu);
     g_live.insert(c.get());
@@ -488,7 +488,7 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
   const int64_t S = (n + ctx->world - 1) / ctx->world;
   const int64_t n_alloc = S * ctx->world;
   const double* Vd = stage_in(ctx, "api.V", V, cols->n, t, cols->n, flags);
-  double* od = (flags & LGP_DEVICE_PTRS) && ctx->world == 1
+  double* od = (flags & LGP_DEVICE_PTRS) && !ctx->sharded()
                    ? out
                    : (double*)ctx->scratch_get("api.out", (size_t)n_alloc * t * 8);
   if (cols->n == 0) {
@@ -507,7 +507,7 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
     op.tag = "api.mv";
     op.prepare();
     op.run(Vd, od + r0 * t, square ? noise : 0.0, square ? Vd + r0 * t : nullptr, nullptr);
-    if (ctx->world > 1) comm_allgather_inplace(ctx->comm, od, (size_t)S * t, ctx->stream);
+    if (ctx->sharded()) comm_allgather_inplace(ctx->comm, od, (size_t)S * t, ctx->stream);
   }
   stage_out(ctx, out, od, (size_t)n * t * 8, flags);
   LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));

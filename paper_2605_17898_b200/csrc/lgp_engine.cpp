@@ -106,7 +106,7 @@ void MatvecOp::prepare() {
   // column partials: one 64-column record per (row block, chunk) pair, n^2/8192
   // records of 512 B - bounded (N <= ~1.1M) so they fit comfortably in HBM
   const double tcsym_bytes = (double)rows->n * (double)rows->n / 8192.0 * 512.0;
-  if (t == 1 && rows == cols && ctx->world == 1 && row0 == 0 && n_rows == rows->n &&
+  if (t == 1 && rows == cols && !ctx->sharded() && row0 == 0 && n_rows == rows->n &&
       tcsym_bytes <= kSymPartialBudget &&
       !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && !std::getenv("LGP_NO_TCSYM")) {
     Plan p = make_tc_plan(k->tree, rows->d, 16, flags);
@@ -234,7 +234,7 @@ void MatvecOp::prepare() {
   const double sym_bytes = (double)n_rb * (n_rb + 1) / 2.0 * rows_per_cta * 16.0 * n_pass * tb;
   // (and enough block pairs to fill the GPU: small operators take the plain
   // kernel, whose column segments supply the parallelism)
-  sym = (rows == cols) && ctx->world == 1 && tb == 1 && !(flags & LGP_NO_SYM) &&
+  sym = (rows == cols) && !ctx->sharded() && tb == 1 && !(flags & LGP_NO_SYM) &&
         (rows_per_cta % tu.cc) == 0 && (int64_t)n_rb * (n_rb + 1) / 2 >= 2 * ctx->sm_count &&
         sym_bytes <= kSymPartialBudget;
   if (sym) {
@@ -491,7 +491,7 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   for (int it = 1; it <= max_iter && !done_h; ++it) {
     op.run(b.p, b.ap + r0 * t, noise, b.p + r0 * t, b.s.done);
-    if (ctx->world > 1) comm_allgather_inplace(ctx->comm, b.ap, (size_t)S * t, ctx->stream);
+    if (ctx->sharded()) comm_allgather_inplace(ctx->comm, b.ap, (size_t)S * t, ctx->stream);
     vec::dot_partial(ctx, b.p, b.ap, n, t, b.part, b.s.done);
     vec::cg_fin_pap(ctx, b.part, nblk, t, b.s);
     vec::cg_update_xr(ctx, b.x, b.r, b.p, b.ap, n, t, b.s, b.part);
@@ -569,7 +569,7 @@ void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, doub
     double* q = basis + (size_t)j * stride;
     const double* qprev = j > 0 ? basis + (size_t)(j - 1) * stride : nullptr;
     op.run(q, w + r0 * t, noise, q + r0 * t, s.done);
-    if (ctx->world > 1) comm_allgather_inplace(ctx->comm, w, (size_t)S * t, ctx->stream);
+    if (ctx->sharded()) comm_allgather_inplace(ctx->comm, w, (size_t)S * t, ctx->stream);
     vec::dot_partial(ctx, q, w, n, t, part, s.done);
     vec::lz_fin_alpha(ctx, part, nblk, t, j, steps, s);
     vec::lz_update1(ctx, w, q, qprev, n, t, j, steps, s);

@@ -154,6 +154,10 @@ struct Context {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   Comm* comm = nullptr;
+  // row-sharded schedule (local rows + NCCL all-gather): every multi-rank
+  // context, and a one-rank context opened with an NCCL id (GPU test of the
+  // sharded path on one device)
+  bool sharded() const { return comm != nullptr; }
   std::recursive_mutex mu;
   std::map<std::string, std::unique_ptr<Module>> modules;
   std::map<std::string, DeviceBuffer> scratch;
