@@ -57,13 +57,36 @@ void require(bool ok, int code, const std::string& msg) {
   if (!ok) throw Error(code, msg);
 }
 
+// Multithreaded finiteness scan (up to 8 threads, >= 2 MB each): a double is
+// finite iff its exponent field is not all ones; (u & m) + 2^52 carries into
+// bit 63 exactly then. Adds and ORs vectorise with baseline SSE2.
+bool all_finite_mt(const double* p, size_t n) {
+  auto scan = [p](size_t lo, size_t hi) {
+    const uint64_t* u = reinterpret_cast<const uint64_t*>(p);
+    const uint64_t m = 0x7ff0000000000000ull;
+    uint64_t acc = 0;
+    for (size_t i = lo; i < hi; ++i) acc |= (u[i] & m) + (uint64_t(1) << 52);
+    return (acc >> 63) != 0;
+  };
+  const size_t kPerThread = size_t(1) << 18;
+  unsigned nt = std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency()));
+  nt = (unsigned)std::min<size_t>(nt, (n + kPerThread - 1) / kPerThread);
+  if (nt <= 1) return !scan(0, n);
+  std::vector<char> flags(nt, 0);
+  std::vector<std::thread> th;
+  const size_t step = (n + nt - 1) / nt;
+  for (unsigned k = 1; k < nt; ++k)
+    th.emplace_back([&, k] { flags[k] = scan(std::min(n, k * step), std::min(n, (k + 1) * step)); });
+  flags[0] = scan(0, std::min(n, step));
+  for (auto& x : th) x.join();
+  for (char f : flags)
+    if (f) return false;
+  return true;
+}
+
 void check_finite(const double* p, size_t n, const char* name) {
-  // branch-free scan (vectorises): a double is finite iff its exponent is not all ones
-  const uint64_t* u = reinterpret_cast<const uint64_t*>(p);
-  const uint64_t m = 0x7ff0000000000000ull;
-  uint64_t bad = 0;
-  for (size_t i = 0; i < n; ++i) bad |= (uint64_t)((u[i] & m) == m);
-  if (bad) throw Error(LGP_E_NONFINITE, std::string(name) + " contains NaN or infinite entries");
+  if (!all_finite_mt(p, n))
+    throw Error(LGP_E_NONFINITE, std::string(name) + " contains NaN or infinite entries");
 }
 
 // Stage a host or device input (n x t) into a device buffer of n_alloc rows.
@@ -287,33 +310,7 @@ int lgp_memcpy_d2h(lgp_ctx* ctx, void* dst, const void* src, size_t bytes) {
 int lgp_all_finite(const double* p, size_t n, int* all_finite) {
   API_BEGIN
   require(all_finite && (n == 0 || p), LGP_E_ARG, "bad lgp_all_finite arguments");
-  // a double is finite iff its exponent field is not all ones; branch-free OR
-  // (u & m) + 2^52 carries into bit 63 exactly when the exponent is all ones;
-  // adds and ORs vectorise with baseline SSE2
-  auto scan = [p](size_t lo, size_t hi) {
-    const uint64_t* u = reinterpret_cast<const uint64_t*>(p);
-    const uint64_t m = 0x7ff0000000000000ull;
-    uint64_t acc = 0;
-    for (size_t i = lo; i < hi; ++i) acc |= (u[i] & m) + (uint64_t(1) << 52);
-    return (acc >> 63) != 0;
-  };
-  const size_t kPerThread = size_t(1) << 18;  // 2 MB per thread and more
-  unsigned nt = std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency()));
-  nt = (unsigned)std::min<size_t>(nt, (n + kPerThread - 1) / kPerThread);
-  bool bad = false;
-  if (nt <= 1) {
-    bad = scan(0, n);
-  } else {
-    std::vector<char> flags(nt, 0);
-    std::vector<std::thread> th;
-    const size_t step = (n + nt - 1) / nt;
-    for (unsigned k = 1; k < nt; ++k)
-      th.emplace_back([&, k] { flags[k] = scan(std::min(n, k * step), std::min(n, (k + 1) * step)); });
-    flags[0] = scan(0, std::min(n, step));
-    for (auto& x : th) x.join();
-    for (char f : flags) bad |= f != 0;
-  }
-  *all_finite = bad ? 0 : 1;
+  *all_finite = all_finite_mt(p, n) ? 1 : 0;
   API_END
 }
 
@@ -477,7 +474,6 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
   require(t >= 1, LGP_E_ARG, "t must be at least 1");
   require(std::isfinite(noise) && noise >= 0.0, LGP_E_ARG, "noise must be finite and nonnegative");
   require(cols->n == 0 || V, LGP_E_ARG, "V is null");
-  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(V, (size_t)cols->n * t, "V");
   std::lock_guard<std::recursive_mutex> g(ctx->mu);
   ctx->activate();
   const bool square = (rows == cols);
@@ -488,6 +484,9 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
   const int64_t S = (n + ctx->world - 1) / ctx->world;
   const int64_t n_alloc = S * ctx->world;
   const double* Vd = stage_in(ctx, "api.V", V, cols->n, t, cols->n, flags);
+  // validate V on the host while its copy is in flight (pinned V: the DMA and
+  // the scan overlap); a non-finite V throws before any kernel is launched
+  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(V, (size_t)cols->n * t, "V");
   double* od = (flags & LGP_DEVICE_PTRS) && !ctx->sharded()
                    ? out
                    : (double*)ctx->scratch_get("api.out", (size_t)n_alloc * t * 8);
@@ -524,12 +523,12 @@ int lgp_cg(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* pts, double nois
   require(std::isfinite(noise) && noise >= 0.0, LGP_E_ARG, "noise must be finite and nonnegative");
   const int64_t n = pts->n;
   require(n >= 1, LGP_E_DIM, "need at least one point");
-  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(B, (size_t)n * t, "b");
   std::lock_guard<std::recursive_mutex> g(ctx->mu);
   ctx->activate();
   const int64_t S = (n + ctx->world - 1) / ctx->world;
   const int64_t n_alloc = S * ctx->world;
   const double* Bd = stage_in(ctx, "api.B", B, n, t, n_alloc, flags);
+  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(B, (size_t)n * t, "b");  // during the copy
   double* xd = nullptr;
   cg_device(ctx, k, pts, noise, Bd, t, rel_tol, max_iter, &xd, iters_out, final_res_out);
   stage_out(ctx, X_out, xd, (size_t)n * t * 8, flags);
@@ -547,12 +546,12 @@ int lgp_lanczos(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* pts, double
   const int64_t n = pts->n;
   require(n >= 1, LGP_E_DIM, "need at least one point");
   require(steps <= n, LGP_E_ARG, "steps must not exceed n");
-  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(Z, (size_t)n * t, "z");
   std::lock_guard<std::recursive_mutex> g(ctx->mu);
   ctx->activate();
   const int64_t S = (n + ctx->world - 1) / ctx->world;
   const int64_t n_alloc = S * ctx->world;
   const double* Zd = stage_in(ctx, "api.Z", Z, n, t, n_alloc, flags);
+  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(Z, (size_t)n * t, "z");  // during the copy
   lanczos_device(ctx, k, pts, noise, Zd, t, steps, alphas, betas, steps_out);
   API_END
 }

@@ -60,12 +60,14 @@ def _finite(a, name):
         raise NonFiniteError(f"{name} contains NaN or infinite entries")
 
 
-def as_matrix(x, name="matrix"):
-    """Finite 2-d float64, C-contiguous (linalg.py:91-97)."""
+def as_matrix(x, name="matrix", check=True):
+    """Finite 2-d float64, C-contiguous (linalg.py:91-97). ``check=False``
+    defers the finiteness scan to the caller (see solvers.matrix_free_matvec)."""
     a = np.asarray(x, dtype=np.float64)
     if a.ndim != 2:
         raise DimensionMismatchError(f"{name} must be 2-d, got ndim={a.ndim}")
-    _finite(a, name)
+    if check:
+        _finite(a, name)
     return np.ascontiguousarray(a)
 
 
@@ -78,10 +80,11 @@ def as_vector(x, name="vector"):
     return np.ascontiguousarray(a)
 
 
-def as_block(x, name="block"):
+def as_block(x, name="block", check=True):
     """Finite 1-d or 2-d float64 (the multi-RHS extension: n x t)."""
     a = np.asarray(x, dtype=np.float64)
     if a.ndim not in (1, 2):
         raise DimensionMismatchError(f"{name} must be 1-d or 2-d, got ndim={a.ndim}")
-    _finite(a, name)
+    if check:
+        _finite(a, name)
     return np.ascontiguousarray(a)

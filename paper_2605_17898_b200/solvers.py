@@ -29,7 +29,7 @@ import scipy.linalg
 from . import _lib
 from .errors import DimensionMismatchError, OperatorNotSpdError
 from .kernels import program, slab_buffer_count
-from .linalg import as_block, as_matrix, as_vector, tracked
+from .linalg import _finite, as_block, as_matrix, as_vector, tracked
 
 
 @dataclass
@@ -80,14 +80,15 @@ class KernelOperator:
             raise DimensionMismatchError(f"v has length {v.shape[0]}, X has {self.n} rows")
         return self._matvec(v)
 
-    def _matvec(self, v):
-        # v: validated (finite, float64, C-contiguous) with n rows
+    def _matvec(self, v, finite=True):
+        # v: float64, C-contiguous, n rows; finite=False: the library checks v
+        # on the host during its copy to the device (NonFiniteError)
         t = 1 if v.ndim == 1 else v.shape[1]
         out = _lib.result_buffer(v.shape)
         if self.n and t:
             _lib.check(_lib.lib().lgp_matvec(self.ctx.handle, self.prog.handle, self.points.handle,
                                              self.points.handle, self.noise, _lib.vptr(v), t,
-                                             _lib.vptr(out), _lib.INPUTS_FINITE))
+                                             _lib.vptr(out), _lib.INPUTS_FINITE if finite else 0))
         return tracked(out)
 
     __call__ = matvec
@@ -125,18 +126,41 @@ def matrix_free_matvec(kernel, x, noise, v, block=256):
     registers; device memory stays O(N * t). ``v`` is an N-vector or an
     N x t block of right-hand sides.
     """
-    x = as_matrix(x, "X")
-    v = as_block(v, "v")
+    # Finiteness: the reference checks X, then v, before anything else
+    # (linalg.py:91-106). On the success path of a large call the scans move
+    # into the library, off the critical path: X is checked on the device
+    # during its upload (point statistics), v on the host while its
+    # host->device copy is in flight. Every error branch below runs the host
+    # scans first, so the reference's error order is kept.
+    x = as_matrix(x, "X", check=False)
+    v = as_block(v, "v", check=False)
+    defer = x.size + v.size >= (1 << 18)
+
+    def scans():
+        _finite(x, "X")
+        _finite(v, "v")
+
+    if not defer:
+        scans()
     n = x.shape[0]
     if v.shape[0] != n:
+        scans()
         raise DimensionMismatchError(f"v has length {v.shape[0]}, X has {n} rows")
     noise = float(noise)
     if not np.isfinite(noise) or noise < 0:
+        scans()
         raise ValueError("noise must be finite and nonnegative")
     if block < 1:
+        scans()
         raise ValueError("block must be at least 1")
-    slab_buffer_count(kernel)  # node-protocol check, as the reference does per call
-    return KernelOperator(kernel, x, noise, _validated=True)._matvec(v)
+    try:
+        slab_buffer_count(kernel)  # node-protocol check, as the reference does per call
+        op = KernelOperator(kernel, x, noise, _validated=True)
+    except Exception:
+        if defer:
+            scans()  # NonFiniteError takes precedence, as in the reference
+        raise
+    return op._matvec(v, finite=not defer)
 
 
 def cg_solve(apply, b, config=None):

@@ -352,3 +352,31 @@ def test_tensor_core_variants_parity(gpu_ctx, monkeypatch, env):
     V = rng.standard_normal((3001, 16))
     got = _mv_flags(expr, x, V, 0.1, 0)
     assert rel_l2(got, O.matvec(O.parse_tree(expr), x, 0.1, V)) <= TOL
+
+
+def test_deferred_validation_large_inputs(gpu_ctx):
+    """Large calls validate X on the device during its upload and v on the
+    host during its copy; the reference's error types and order still hold."""
+    rng = np.random.default_rng(8)
+    n = 70000
+    x = rng.random((n, 4))
+    v = rng.standard_normal(n)
+    k = G.RBF(0.7)
+    bad_x = x.copy()
+    bad_x[123, 2] = np.nan
+    bad_v = v.copy()
+    bad_v[10] = np.inf
+    with pytest.raises(G.NonFiniteError, match="X"):
+        G.matrix_free_matvec(k, bad_x, 0.1, v)
+    with pytest.raises(G.NonFiniteError):
+        G.matrix_free_matvec(k, x, 0.1, bad_v)
+    with pytest.raises(G.NonFiniteError, match="X"):  # X before v, before the length check
+        G.matrix_free_matvec(k, bad_x, 0.1, bad_v[:-5])
+    with pytest.raises(G.NonFiniteError):  # v before the length check
+        G.matrix_free_matvec(k, x, 0.1, bad_v[:-5])
+    with pytest.raises(G.DimensionMismatchError):
+        G.matrix_free_matvec(k, x, 0.1, v[:-5])
+    with pytest.raises(G.NonFiniteError):  # before the noise check
+        G.matrix_free_matvec(k, x, -1.0, bad_v)
+    good = G.matrix_free_matvec(k, x, 0.1, v)
+    assert np.isfinite(good).all()
