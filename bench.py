@@ -27,6 +27,7 @@ sample of the same workload per step, on rank 0 only.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import datetime
 import json
 import os
@@ -141,6 +142,20 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+@contextlib.contextmanager
+def stdout_to_stderr():
+    """Route file descriptor 1 to stderr (native libraries printing at init)."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 def dist_setup(world):
     if world <= 1:
         return None
@@ -240,11 +255,13 @@ def run_reference(args, rank, world):
     return 0
 
 
-def workload_config(name, cfg):
+def workload_config(name, cfg, world=1, sharded=False):
+    par = (f"row-sharded K over {world} rank(s), NCCL all-gather" if (world > 1 or sharded)
+           else "one GPU (all rows of K)")
     return {"workload": f"{name}: (K+{cfg['noise']}I)V, kernel {cfg['kernel']}, N={cfg['n']}, "
                         f"D={cfg['d']}, t={cfg['t']} SLQ probe vectors",
             "n": cfg["n"], "d": cfg["d"], "t": cfg["t"], "kernel": cfg["kernel"],
-            "noise": cfg["noise"], "parallelism": "row-sharded K, NCCL all-gather",
+            "noise": cfg["noise"], "parallelism": par,
             "l2": "flushed (256 MiB memset) before every timed step"}
 
 
@@ -256,7 +273,12 @@ def run_ours(args, rank, world):
     from oracle import gp_oracle as O  # input recipe + CPU baseline only
 
     dist = dist_setup(world)
-    ctx = distributed.init() if world > 1 else _lib.default_context()
+    # rank 0 prints exactly one JSON line on stdout: NCCL's own log lines
+    # ("NCCL version ...") go to stderr
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    with stdout_to_stderr():
+        ctx = distributed.init(force_comm=args.sharded) if (world > 1 or args.sharded) \
+            else _lib.default_context()
     lib = _lib.lib()
     cfg = dict(O.CONFIGS[args.config])
     n, d, t = cfg["n"], cfg["d"], cfg["t"]
@@ -424,7 +446,7 @@ def run_ours(args, rank, world):
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 entries / f64 accumulate", "data": "synthetic",
-            "config": workload_config(args.config, cfg),
+            "config": workload_config(args.config, cfg, world, args.sharded),
             "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "parity_rel_l2": parity}
     line.update(solve)
@@ -443,6 +465,9 @@ def main():
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="row-sharded schedule with an NCCL communicator even at one rank "
+                         "(exercises the multi-GPU path on one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", "0"))

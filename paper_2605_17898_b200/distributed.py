@@ -15,14 +15,21 @@ import os
 from . import _lib
 
 
-def init(device=None):
+def init(device=None, force_comm=False):
+    """This rank's context; ``force_comm`` opens a one-rank NCCL communicator
+    at world 1 so the row-sharded schedule runs on a single GPU."""
     import torch.distributed as dist
 
     rank = dist.get_rank() if dist.is_initialized() else int(os.environ.get("RANK", "0"))
     world = dist.get_world_size() if dist.is_initialized() else int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", rank)) if device is None else int(device)
     if world == 1:
-        ctx = _lib.Context(local)
+        if force_comm:
+            buf = C.create_string_buffer(128)
+            _lib.check(_lib.lib().lgp_comm_unique_id(buf))
+            ctx = _lib.Context(local, 0, 1, buf.raw)
+        else:
+            ctx = _lib.Context(local)
     else:
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed must be initialised for a multi-rank context")
