@@ -7,8 +7,14 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
+#include <string>
+#include <vector>
 
 #include "lgp_internal.h"
 
@@ -54,9 +60,43 @@ void check(ncclResult_t r, const char* what) {
 }
 }  // namespace
 
+// Loopback group (TEST ONLY): the ranks of one process, each with its own
+// context / stream on the same GPU, run by host threads. The all-gather is
+// host-mediated (stream sync, host barrier, device-to-device copies of the
+// peers' slices, barrier): no kernel ever waits on another rank, so the ranks
+// need not be co-scheduled. It exercises the engine's multi-rank bookkeeping
+// (row partitions, padded slices, offsets) on one GPU. Selected by an id whose
+// first 12 bytes are "LGP-LOOPBACK"; bytes 12.. name the group.
+namespace {
+constexpr char kLoopMagic[] = "LGP-LOOPBACK";
+struct Loopback {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long gen = 0;
+  std::vector<double*> bufs;
+  void barrier() {
+    std::unique_lock<std::mutex> l(mu);
+    const long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    if (!cv.wait_for(l, std::chrono::seconds(120), [&] { return gen != g; }))
+      throw Error(LGP_E_NCCL, "loopback all-gather: a rank did not arrive within 120 s");
+  }
+};
+std::mutex g_loop_mu;
+std::map<std::string, std::weak_ptr<Loopback>> g_loop;
+}  // namespace
+
 struct Comm {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  std::shared_ptr<Loopback> loop;
 };
 
 void comm_unique_id(uint8_t* out128) {
@@ -68,6 +108,23 @@ void comm_unique_id(uint8_t* out128) {
 
 Comm* comm_create(int rank, int world, const uint8_t* id128, cudaStream_t stream) {
   (void)stream;
+  if (std::memcmp(id128, kLoopMagic, sizeof(kLoopMagic) - 1) == 0) {
+    const std::string key(reinterpret_cast<const char*>(id128), 128);
+    std::lock_guard<std::mutex> g(g_loop_mu);
+    std::shared_ptr<Loopback> lb = g_loop[key].lock();
+    if (!lb) {
+      lb = std::make_shared<Loopback>();
+      lb->world = world;
+      lb->bufs.assign(world, nullptr);
+      g_loop[key] = lb;
+    }
+    if (lb->world != world) throw Error(LGP_E_ARG, "loopback group world size mismatch");
+    Comm* c = new Comm;
+    c->rank = rank;
+    c->world = world;
+    c->loop = lb;
+    return c;
+  }
   ncclUniqueId id;
   std::memcpy(&id, id128, 128);
   Comm* c = new Comm;
@@ -83,11 +140,27 @@ Comm* comm_create(int rank, int world, const uint8_t* id128, cudaStream_t stream
 
 void comm_destroy(Comm* c) {
   if (!c) return;
-  if (c->comm && api().comm_destroy) api().comm_destroy(c->comm);
+  if (c->comm && !c->loop && api().comm_destroy) api().comm_destroy(c->comm);
   delete c;
 }
 
 void comm_allgather_inplace(Comm* c, double* buf, size_t count, cudaStream_t stream) {
+  if (c->loop) {
+    Loopback& lb = *c->loop;
+    {
+      std::lock_guard<std::mutex> g(lb.mu);
+      lb.bufs[c->rank] = buf;
+    }
+    LGP_CUDA_CHECK(cudaStreamSynchronize(stream));  // own slice written
+    lb.barrier();                                   // every slice written, every buffer known
+    for (int q = 0; q < c->world; ++q)
+      if (q != c->rank)
+        LGP_CUDA_CHECK(cudaMemcpyAsync(buf + (size_t)q * count, lb.bufs[q] + (size_t)q * count,
+                                       count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    LGP_CUDA_CHECK(cudaStreamSynchronize(stream));
+    lb.barrier();  // every peer has read this rank's slice
+    return;
+  }
   check(api().all_gather(buf + (size_t)c->rank * count, buf, count, ncclFloat64, c->comm, stream),
         "ncclAllGather");
 }
