@@ -94,7 +94,10 @@ int lgp_partition(int64_t n, int world, int rank, int64_t* r0, int64_t* r1);
 int lgp_comm_unique_id(uint8_t* out128);
 /* world == 1: nccl_id may be NULL (no communicator). A non-NULL id at world 1
  * opens a one-rank NCCL communicator and runs the row-sharded schedule
- * (device coverage of the multi-GPU path on one GPU). */
+ * (device coverage of the multi-GPU path on one GPU). TEST ONLY: an id whose
+ * first 12 bytes are "LGP-LOOPBACK" makes the ranks of one process (host
+ * threads, one context each, same GPU) a loopback group with host-mediated
+ * gathers (tests/test_gpu_loopback.py). */
 int lgp_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, lgp_ctx** out);
 int lgp_ctx_destroy(lgp_ctx* ctx);
 int lgp_ctx_sync(lgp_ctx* ctx);
