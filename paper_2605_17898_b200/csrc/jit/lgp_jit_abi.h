@@ -85,6 +85,8 @@ struct LgpTcSymArgs {
   const float* a1;            // row operand tiles (FP16 hi/lo features) [n_rb][128 x KD]
   const float* b1;            // column operand tiles [n_tiles][64 x KD]
   const double* v;            // RHS, zero-padded to the column padding (t = 1)
+  const float* r32;           // FP32 row features [n_rows_pad][FW] (Periodic trees; else null)
+  const float* c32;           // FP32 column features [n_cols_pad][FW] (Periodic trees; else null)
   const int* items;           // [n_items][3]: row block I, chunk range [c0, c1)
   const long long* colbase;   // [n_rb]: first column-partial record of row block I
   double* rowpart;            // [n_items][128]

@@ -97,8 +97,14 @@
 #ifndef LGP_TC_SIMT_MASK
 #define LGP_TC_SIMT_MASK 0
 #endif
-// FP32 column features of a chunk (staged only for FMA-pipe distance chunks)
-#define TC_C32_BYTES (LGP_TC_SIMT_MASK ? TC_CH * LGP_TC_FW * 4 : 0)
+#ifndef LGP_TC_PF
+#define LGP_TC_PF 0  // Periodic (cos, sin) features per point, from offset LGP_TC_P0
+#define LGP_TC_P0 0
+#endif
+// FP32 column features of a chunk (staged for FMA-pipe distance chunks, and
+// for every chunk when the tree has Periodic leaves)
+#define TC_C32_BYTES ((LGP_TC_SIMT_MASK || LGP_TC_PF) ? TC_CH * LGP_TC_FW * 4 : 0)
+#define TC_C32(c) (TC_SIMT(c) || LGP_TC_PF > 0)
 #define TC_STAGE_BYTES (TC_B1H_BYTES + TC_VH_BYTES + TC_C32_BYTES)
 #if LGP_TC_PAIR && LGP_TC_SIMT_MASK
 #error "FMA-pipe distance chunks are single-CTA only"
@@ -514,6 +520,9 @@ extern "C" __global__ void lgp_tc_prep(LgpPrepArgs p, int tile_rows, int is_col)
       f[LGP_D] = (float)(-nn);
 #pragma unroll
       for (int k = LGP_D + 1; k < LGP_TC_FW; ++k) f[k] = 0.f;
+#if LGP_TC_PF
+      lgp_tc_prep_feat(x, p, f + LGP_TC_P0);
+#endif
     }
   } else if (p.f32 != nullptr) {
 #pragma unroll
@@ -638,7 +647,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
         TR_MARK(0)
         const unsigned dst = lgp_saddr(stg + (size_t)s * TC_STAGE_BYTES);
         lgp_mbar_expect_tx(BAR(B_SFULL(s)),
-                           TC_B1H_BYTES + TC_VH_BYTES + (TC_SIMT(c) ? TC_C32_BYTES : 0));
+                           TC_B1H_BYTES + TC_VH_BYTES + (TC_C32(c) ? TC_C32_BYTES : 0));
         lgp_bulk_g2s(dst,
                      reinterpret_cast<const unsigned char*>(a.b1) +
                          (size_t)(tile0 + c) * TC_B1_BYTES + rank * TC_B1H_BYTES,
@@ -647,7 +656,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
                      vbase + ((size_t)pass * a.n_tiles + tile0 + c) * TC_V_BYTES +
                          rank * TC_VH_BYTES,
                      TC_VH_BYTES, BAR(B_SFULL(s)));
-        if (TC_SIMT(c))
+        if (TC_C32(c))
           lgp_bulk_g2s(dst + TC_B1H_BYTES + TC_VH_BYTES,
                        reinterpret_cast<const unsigned char*>(a.c32) +
                            (size_t)(tile0 + c) * TC_C32_BYTES,
@@ -778,6 +787,12 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
     for (int d = 0; d <= LGP_D; ++d) rf32[d] = a.r32[((size_t)rb * 128 + row) * LGP_TC_FW + d];
 #endif
+#if LGP_TC_PF
+    float frp[LGP_TC_PF];  // this thread's row: Periodic (cos, sin) features
+#pragma unroll
+    for (int f = 0; f < LGP_TC_PF; ++f)
+      frp[f] = a.r32[((size_t)rb * 128 + row) * LGP_TC_FW + LGP_TC_P0 + f];
+#endif
 
     auto drain = [&](int gi) {
       const int b = gi & 1;
@@ -902,14 +917,26 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
         lgp_tmem_ld32p(sb + 32u, s + 32);
         lgp_tmem_wait_ld();
       }
+#if LGP_TC_PF
+      // column Periodic features of this chunk, staged with its B tile (the
+      // stage is released only after this chunk's contraction)
+      const int cpf = 2 * k + w;
+      lgp_mbar_wait(BAR(B_SFULL(cpf % LGP_TC_STAGES)), (cpf / LGP_TC_STAGES) & 1);
+      const float* cfp = reinterpret_cast<const float*>(stg + (size_t)(cpf % LGP_TC_STAGES) * TC_STAGE_BYTES +
+                                                        TC_B1H_BYTES + TC_VH_BYTES) + LGP_TC_P0;
+#define TC_KJ(x, pxv, j) lgp_tc_kf((x), a, (pxv), frp, cfp + (j) * LGP_TC_FW)
+#else
+#define TC_KJ(x, pxv, j) lgp_tc_k((x), a, (pxv))
+#endif
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
         const int px = (m & 7) < (LGP_TC_POLY + 1) / 2 ? 1 : 0;
         const int px1 = (m & 7) < LGP_TC_POLY / 2 ? 1 : 0;
-        const float k0 = lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(s[2 * m])), a, px);
-        const float k1 = lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(s[2 * m + 1])), a, px1);
+        const float k0 = TC_KJ(LGP_TC_CLAMP(__uint_as_float(s[2 * m])), px, 2 * m);
+        const float k1 = TC_KJ(LGP_TC_CLAMP(__uint_as_float(s[2 * m + 1])), px1, 2 * m + 1);
         lgp_split_f16x2(k0, k1, s[2 * m], s[2 * m + 1]);
       }
+#undef TC_KJ
       lgp_tmem_st32s2(sb, s);        // hi pairs -> columns 0..31
       lgp_tmem_st32s2(sb + 32u, s + 1);  // lo pairs -> columns 32..63
       }

@@ -53,7 +53,11 @@
 #endif
 #define TS_NSBW (LGP_TS_NSB / LGP_TS_NWG)    // S buffers per warpgroup
 #define TS_VCH_BYTES (TC_CH * 8)                        // p chunk, FP64
-#define TS_STAGE_BYTES (TC_B1_BYTES + TS_VCH_BYTES)
+#define TS_F32_BYTES (LGP_TC_PF ? TC_CH * LGP_TC_FW * 4 : 0)  // column Periodic features
+#define TS_STAGE_BYTES (TC_B1_BYTES + TS_VCH_BYTES + TS_F32_BYTES)
+#if LGP_TC_PF && LGP_TS_LAYOUT != 1
+#error "Periodic features need the 16x256b epilogue layout"
+#endif
 #define TS_CBUF_BYTES (LGP_TS_NWG * 2 * 4 * TC_CH * 8)  // [wg][parity][warp][64] FP64
 #define TS_NBARS (1 + 2 * LGP_TC_STAGES + 2 * LGP_TS_NSB)
 #define TSB_AFULL 0
@@ -161,6 +165,10 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
                      TC_B1_BYTES, TBAR(TSB_SFULL(s)));
         lgp_bulk_g2s(dst + TC_B1_BYTES, a.v + (size_t)(c0 + c) * TC_CH, TS_VCH_BYTES,
                      TBAR(TSB_SFULL(s)));
+#if LGP_TC_PF
+        lgp_bulk_g2s(dst + TC_B1_BYTES + TS_VCH_BYTES, a.c32 + (size_t)(c0 + c) * TC_CH * LGP_TC_FW,
+                     TS_F32_BYTES, TBAR(TSB_SFULL(s)));
+#endif
       }
     }
     __syncwarp();
@@ -207,6 +215,18 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
       vi[u] = vis[32 * q4 + 16 * (u >> 1) + 8 * (u & 1) + r0];
       acc[u] = 0.0;
     }
+#if LGP_TC_PF
+    float frp[4][LGP_TC_PF];  // Periodic features of the thread's 4 rows
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int f = 0; f < LGP_TC_PF; ++f)
+        frp[u][f] = a.r32[(size_t)(128 * I + 32 * q4 + 16 * (u >> 1) + 8 * (u & 1) + r0) * LGP_TC_FW +
+                          LGP_TC_P0 + f];
+#define TS_KJ(x, px, u, j) lgp_tc_kf((x), a, (px), frp[u], cfp + (j) * LGP_TC_FW)
+#else
+#define TS_KJ(x, px, u, j) lgp_tc_k((x), a, (px))
+#endif
     // after the butterfly lane t holds column 8 k + 2 cq + e, k = 2 b4 + b3, e = b2
     const int ccol = 8 * (2 * ((lane >> 4) & 1) + ((lane >> 3) & 1)) + 2 * cq + ((lane >> 2) & 1);
     for (int k = 0; k < nloc; ++k) {
@@ -218,6 +238,10 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
       lgp_tc_fence_after();
       lgp_mbar_wait(TBAR(TSB_SFULL(s)), (c / LGP_TC_STAGES) & 1);  // p chunk visible
       const double* vj = reinterpret_cast<const double*>(stg + (size_t)s * TS_STAGE_BYTES + TC_B1_BYTES);
+#if LGP_TC_PF
+      const float* cfp = reinterpret_cast<const float*>(stg + (size_t)s * TS_STAGE_BYTES + TC_B1_BYTES +
+                                                        TS_VCH_BYTES) + LGP_TC_P0;
+#endif
       const bool diag = chunk < 2 * I + 2;
       // diagonal chunks: column offset relative to this thread's first row
       const int dj0 = chunk * TC_CH - (128 * I + 32 * q4 + r0) + 2 * cq;
@@ -274,7 +298,9 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
 #if (LGP_TS_ABLATE & 2)
               const double kd = lgp_widen_nn(__uint_as_float(sv[h][r]) * 0.5f);
 #else
-              const double kd = lgp_widen_nn(lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[h][r])), a, r < LGP_TS_POLY ? 1 : 0));
+              const double kd = lgp_widen_nn(TS_KJ(LGP_TC_CLAMP(__uint_as_float(sv[h][r])),
+                                                   r < LGP_TS_POLY ? 1 : 0, u,
+                                                   32 * g + 8 * (r >> 2) + 2 * cq + (r & 1)));
 #endif
               acc[u] = fma(kd, pj[m], acc[u]);
               cv[m] = fma(kd, vi[u], cv[m]);
@@ -287,7 +313,7 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
             for (int r = 0; r < 16; ++r) {
               const int b = r >> 2, e = r & 1;
               const int u = 2 * h + ((r >> 1) & 1), m = 2 * b + e;
-              const float kk = lgp_tc_k(LGP_TC_CLAMP(__uint_as_float(sv[h][r])), a, 0);
+              const float kk = TS_KJ(LGP_TC_CLAMP(__uint_as_float(sv[h][r])), 0, u, 32 * g + 8 * b + 2 * cq + e);
               const int dj = dj0 + 32 * g + 8 * b + e - (16 * h + 8 * ((r >> 1) & 1));  // j - i
               acc[u] = fma(lgp_widen_nn(dj >= 0 ? kk : 0.f), pj[m], acc[u]);
               cv[m] = fma(lgp_widen_nn(dj > 0 ? kk : 0.f), vi[u], cv[m]);

@@ -156,7 +156,7 @@ void MatvecOp::prepare() {
     // operands pre-tiled in the UMMA canonical layout, FP16 hi/lo split
     fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * plan.tc_kd * 2);
     fc = (float*)ctx->scratch_get(tag + ".b1", (size_t)n_cols_pad * plan.tc_kd * 2);
-    if (plan.tc_simt) {
+    if (plan.tc_simt || plan.tc_pf > 0) {
       r32 = (float*)ctx->scratch_get(tag + ".r32", (size_t)n_rows_pad * plan.tc_fw * 4);
       c32 = (float*)ctx->scratch_get(tag + ".c32", (size_t)n_cols_pad * plan.tc_fw * 4);
     }
@@ -311,6 +311,8 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
       a.a1 = fr;
       a.b1 = fc;
       a.v = vpack;
+      a.r32 = r32;
+      a.c32 = c32;
       a.items = items;
       a.colbase = colbase;
       a.rowpart = partial;

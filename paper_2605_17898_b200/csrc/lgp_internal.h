@@ -101,6 +101,7 @@ struct Plan {
   int tc_n = 16;            // RHS per pass (GEMM2 N)
   bool tc_pair = false;     // K1-TC on CTA pairs (cta_group::2, 256-row blocks)
   int tc_fw = 0;            // FP32 features per point for FMA-pipe distance chunks
+  int tc_pf = 0;            // of which Periodic (cos, sin) features, from offset P0
   bool tc_simt = false;     // some K1-TC chunks compute distances on the FMA pipe
   size_t smem_tcsym = 0;    // dynamic shared memory of lgp_matvec_tcsym
   int ts_nwg = 3;           // lgp_matvec_tcsym epilogue warpgroups

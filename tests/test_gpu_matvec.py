@@ -225,7 +225,12 @@ TC_CASES = [("(rbf 0.5)", 300, 8, 16), ("(rbf 0.5)", 1000, 8, 16), ("(matern52 0
             ("(rbf 0.3)", 2000, 8, 16), ("(matern32 0.6)", 1500, 12, 16), ("(rbf 0.5)", 700, 8, 300),
             ("(rbf 2.5)", 900, 40, 16),
             ("(+ (scale 2.0 (rbf 0.4)) (scale 0.5 (matern32 0.9)))", 2049, 6, 20),
-            ("(scale 1.5 (matern32 0.5))", 4096, 8, 16), ("(* (rbf 0.8) (matern52 1.1))", 129, 5, 33)]
+            ("(scale 1.5 (matern32 0.5))", 4096, 8, 16), ("(* (rbf 0.8) (matern52 1.1))", 129, 5, 33),
+            # Periodic leaves: (cos, sin) features staged next to the distance tile
+            ("(+ (scale 1.0 (rbf 0.5)) (scale 1.0 (periodic 1.0 1.0)))", 2049, 2, 16),
+            ("(* (rbf 0.7) (periodic 0.8 1.3))", 1500, 3, 20),
+            ("(+ (matern52 0.6) (scale 0.7 (periodic 1.2 0.7)))", 1000, 5, 8),
+            ("(+ (periodic 0.9 0.6) (* (rbf 1.1) (periodic 1.5 2.0)))", 700, 1, 16)]
 
 
 def _mv_flags(expr, x, V, noise, flags):
@@ -256,7 +261,9 @@ def test_tensor_core_matvec_parity(gpu_ctx, expr, n, d, t, kind):
 
 def test_tensor_core_not_used_where_ineligible():
     for expr, d, t in [("(rbf 0.5)", 8, 1), ("(rbf 0.2)", 1, 16), ("(matern12 0.5)", 8, 16),
-                       ("(+ (rbf 0.5) (periodic 1.0 1.0))", 4, 16), ("(linear 0.5)", 8, 16)]:
+                       ("(periodic 1.0 1.0)", 4, 16), ("(linear 0.5)", 8, 16),
+                       # angle addition too coarse for this lengthscale: direct sin (SIMT)
+                       ("(+ (rbf 0.5) (periodic 0.001 1.0))", 4, 16)]:
         assert "lgp_matvec_tc" not in G.kernels.program(G.parse_kernel(expr)).source(d, t)
 
 

@@ -173,7 +173,8 @@ def test_evidence_optimizer_matches_reference(gpu_ctx):
     np.testing.assert_allclose(best, g["gp_best"], atol=2e-3)
 
 
-@pytest.mark.parametrize("d,expr", [(4, "(matern52 0.7)"), (40, "(rbf 2.5)")])
+@pytest.mark.parametrize("d,expr", [(4, "(matern52 0.7)"), (40, "(rbf 2.5)"),
+                                    (2, "(+ (scale 1.0 (rbf 0.5)) (scale 1.0 (periodic 1.0 1.0)))")])
 def test_symmetric_tensor_core_cg_dims(gpu_ctx, monkeypatch, d, expr):
     """The default CG matvec for r^2 trees (K1-TC-sym) at the smallest and a
     large feature dimension: same iterations / solution as the SIMT kernel."""
