@@ -36,6 +36,9 @@
 #ifndef LGP_TS_ABLATE
 #define LGP_TS_ABLATE 0
 #endif
+#ifndef LGP_TS_RFG
+#define LGP_TS_RFG 0  // 1: Periodic row features through L1 (more spills: 708 vs 248 B)
+#endif
 #ifndef LGP_TS_POLY
 #define LGP_TS_POLY 0  // entries per 16 whose exp2 runs on the FMA pipe (layout 1)
 #endif
@@ -215,7 +218,13 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
       vi[u] = vis[32 * q4 + 16 * (u >> 1) + 8 * (u & 1) + r0];
       acc[u] = 0.0;
     }
-#if LGP_TC_PF
+#if LGP_TC_PF && LGP_TS_RFG
+    // Periodic features of the thread's 4 rows read through L1 at each use
+    // (held in registers they spill: 96 registers at 4 warpgroups)
+    const float* __restrict__ frb = a.r32 + (size_t)(128 * I + 32 * q4 + r0) * LGP_TC_FW + LGP_TC_P0;
+#define TS_KJ(x, px, u, j) \
+  lgp_tc_kf((x), a, (px), frb + (16 * ((u) >> 1) + 8 * ((u) & 1)) * LGP_TC_FW, cfp + (j) * LGP_TC_FW)
+#elif LGP_TC_PF
     float frp[4][LGP_TC_PF];  // Periodic features of the thread's 4 rows
 #pragma unroll
     for (int u = 0; u < 4; ++u)
