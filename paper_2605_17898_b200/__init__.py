@@ -64,6 +64,7 @@ from .models import (
     gp_fit,
     gp_predict,
     log_marginal_likelihood,
+    metrics,
     optimize_hyperparams,
     unflatten_model_params,
 )

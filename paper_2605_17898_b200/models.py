@@ -258,3 +258,22 @@ def exact_evidence_objective(x, y, kernel, cg_config=None, seed=0):
         return log_marginal_likelihood(st, seed=seed)
 
     return objective
+
+
+def metrics(mean, var_latent, noise, y_true):
+    """(rmse, mean negative log predictive density, 95 % coverage) of latent
+    predictions scored against noisy observations (models.py:471-487): the
+    noise variance is added to the latent variance before scoring. Host-side
+    caller of gp_predict's outputs (the JSON server's ``metrics`` op)."""
+    mean = as_vector(mean, "mean")
+    var_latent = as_vector(var_latent, "var")
+    y_true = as_vector(y_true, "y")
+    if not (mean.shape == var_latent.shape == y_true.shape):
+        raise DimensionMismatchError("metrics inputs must share length")
+    s2 = var_latent + float(noise)
+    resid = y_true - mean
+    sq = resid * resid
+    rmse = float(np.sqrt(np.mean(sq)))
+    nll = float(np.mean(0.5 * np.log(2.0 * math.pi * s2) + sq / (2.0 * s2)))
+    cover = float(np.mean(np.abs(resid) <= 1.96 * np.sqrt(s2)))
+    return rmse, nll, cover
