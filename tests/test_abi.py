@@ -80,8 +80,14 @@ def test_jit_compiles_without_spills(expr, d, t):
 
 
 def test_generated_source_mentions_tree():
+    # cfg3's tree at t = 16: tensor-core kernel with staged Periodic features
     src = G.kernels.program(G.parse_kernel("(+ (scale 1.0 (rbf 0.5)) (scale 1.0 (periodic 1.0 1.0)))")).source(2, 16)
+    assert "lgp_matvec_tc" in src and "lgp_tc_prep_feat" in src and "sincos" in src
+    assert "#define LGP_TC_PF 4" in src
+    # a Matern-1/2 tree stays on the SIMT kernel
+    src = G.kernels.program(G.parse_kernel("(+ (scale 1.0 (matern12 0.5)) (periodic 1.0 1.0))")).source(2, 16)
     assert "lgp_ex2" in src and "cp.async.bulk" in src and "#define LGP_TB 16" in src
+    assert "lgp_matvec_tc" not in src
 
 
 def test_no_gpu_fails_loudly():
