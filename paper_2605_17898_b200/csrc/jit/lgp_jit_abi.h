@@ -93,6 +93,8 @@ struct LgpTcSymArgs {
   double* colpart;            // [records][64]: record (I, c) at colbase[I] + c - 2I
   const int* done;            // optional early-exit flag
   unsigned long long* trace;  // LGP_TC_TRACE builds only
+  int item_base;              // first work item of this launch (multi-rank CG: the rank's share)
+  int pad_;
   float kc[LGP_MAX_KC];
 };
 #endif

@@ -107,7 +107,7 @@ __device__ __forceinline__ void lgp_xreduce(double* x, int o, bool up) {
 
 extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(const LgpTcSymArgs a) {
   if (a.done != nullptr && *a.done) return;
-  const int item = blockIdx.x;
+  const int item = a.item_base + (int)blockIdx.x;
   const int I = a.items[3 * item], c0 = a.items[3 * item + 1], c1 = a.items[3 * item + 2];
   const int nch = c1 - c0;
 

@@ -28,6 +28,8 @@ struct NcclApi {
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                              cudaStream_t) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
   const char* (*get_error_string)(ncclResult_t) = nullptr;
 };
 
@@ -45,9 +47,10 @@ NcclApi& api() {
     a.comm_init_rank = (decltype(a.comm_init_rank))dlsym(a.h, "ncclCommInitRank");
     a.comm_destroy = (decltype(a.comm_destroy))dlsym(a.h, "ncclCommDestroy");
     a.all_gather = (decltype(a.all_gather))dlsym(a.h, "ncclAllGather");
+    a.all_reduce = (decltype(a.all_reduce))dlsym(a.h, "ncclAllReduce");
     a.get_error_string = (decltype(a.get_error_string))dlsym(a.h, "ncclGetErrorString");
   });
-  if (!a.h || !a.get_unique_id || !a.comm_init_rank || !a.all_gather)
+  if (!a.h || !a.get_unique_id || !a.comm_init_rank || !a.all_gather || !a.all_reduce)
     throw Error(LGP_E_NCCL, "libnccl.so.2 could not be loaded");
   return a;
 }
@@ -76,6 +79,8 @@ struct Loopback {
   int arrived = 0;
   long gen = 0;
   std::vector<double*> bufs;
+  std::vector<double*> tmp;  // per-rank sum buffers (all-reduce)
+  std::vector<size_t> tmp_n;
   void barrier() {
     std::unique_lock<std::mutex> l(mu);
     const long g = gen;
@@ -116,6 +121,8 @@ Comm* comm_create(int rank, int world, const uint8_t* id128, cudaStream_t stream
       lb = std::make_shared<Loopback>();
       lb->world = world;
       lb->bufs.assign(world, nullptr);
+      lb->tmp.assign(world, nullptr);
+      lb->tmp_n.assign(world, 0);
       g_loop[key] = lb;
     }
     if (lb->world != world) throw Error(LGP_E_ARG, "loopback group world size mismatch");
@@ -140,6 +147,12 @@ Comm* comm_create(int rank, int world, const uint8_t* id128, cudaStream_t stream
 
 void comm_destroy(Comm* c) {
   if (!c) return;
+  if (c->loop) {
+    std::lock_guard<std::mutex> g(c->loop->mu);
+    if (c->loop->tmp[c->rank]) cudaFree(c->loop->tmp[c->rank]);
+    c->loop->tmp[c->rank] = nullptr;
+    c->loop->tmp_n[c->rank] = 0;
+  }
   if (c->comm && !c->loop && api().comm_destroy) api().comm_destroy(c->comm);
   delete c;
 }
@@ -163,6 +176,36 @@ void comm_allgather_inplace(Comm* c, double* buf, size_t count, cudaStream_t str
   }
   check(api().all_gather(buf + (size_t)c->rank * count, buf, count, ncclFloat64, c->comm, stream),
         "ncclAllGather");
+}
+
+void comm_allreduce_sum_inplace(Comm* c, double* buf, size_t count, cudaStream_t stream) {
+  if (c->loop) {
+    // every rank sums all ranks' buffers in rank order into its own scratch
+    // (identical bits everywhere), then copies the sum over its buffer once
+    // no peer reads it any more
+    Loopback& lb = *c->loop;
+    double* tmp = nullptr;
+    {
+      std::lock_guard<std::mutex> g(lb.mu);
+      lb.bufs[c->rank] = buf;
+      if (lb.tmp_n[c->rank] < count) {
+        if (lb.tmp[c->rank]) cudaFree(lb.tmp[c->rank]);
+        LGP_CUDA_CHECK(cudaMalloc(&lb.tmp[c->rank], count * sizeof(double)));
+        lb.tmp_n[c->rank] = count;
+      }
+      tmp = lb.tmp[c->rank];
+    }
+    LGP_CUDA_CHECK(cudaStreamSynchronize(stream));
+    lb.barrier();
+    LGP_CUDA_CHECK(cudaMemcpyAsync(tmp, lb.bufs[0], count * sizeof(double), cudaMemcpyDeviceToDevice,
+                                   stream));
+    for (int q = 1; q < c->world; ++q) vec::add_inplace(tmp, lb.bufs[q], (int64_t)count, stream);
+    LGP_CUDA_CHECK(cudaStreamSynchronize(stream));
+    lb.barrier();
+    LGP_CUDA_CHECK(cudaMemcpyAsync(buf, tmp, count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    return;
+  }
+  check(api().all_reduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, stream), "ncclAllReduce");
 }
 
 }  // namespace lgp

@@ -106,7 +106,7 @@ void MatvecOp::prepare() {
   // column partials: one 64-column record per (row block, chunk) pair, n^2/8192
   // records of 512 B - bounded (N <= ~1.1M) so they fit comfortably in HBM
   const double tcsym_bytes = (double)rows->n * (double)rows->n / 8192.0 * 512.0;
-  if (t == 1 && rows == cols && !ctx->sharded() && row0 == 0 && n_rows == rows->n &&
+  if (t == 1 && rows == cols && (!ctx->sharded() || rank_split) && row0 == 0 && n_rows == rows->n &&
       tcsym_bytes <= kSymPartialBudget &&
       !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && !std::getenv("LGP_NO_TCSYM")) {
     Plan p = make_tc_plan(k->tree, rows->d, 16, flags);
@@ -214,6 +214,22 @@ void MatvecOp::prepare() {
         rec += m;
       }
       n_items = (int)(it.size() / 3);
+      item_lo = 0;
+      item_hi = n_items;
+      if (rank_split && ctx->world > 1) {
+        // contiguous item ranges with (nearly) equal chunk counts per rank
+        int64_t acc = 0, next = 0;
+        int r = 0;
+        std::vector<int> cut(ctx->world + 1, n_items);
+        cut[0] = 0;
+        for (int q = 0; q < n_items; ++q) {
+          while (r < ctx->world - 1 && acc >= (int64_t)(r + 1) * total / ctx->world) cut[++r] = q;
+          acc += it[3 * q + 2] - it[3 * q + 1];
+        }
+        (void)next;
+        item_lo = cut[ctx->rank];
+        item_hi = cut[ctx->rank + 1];
+      }
       items = (int*)ctx->scratch_get(tag + ".items", it.size() * 4);
       colbase = (long long*)ctx->scratch_get(tag + ".colbase", (size_t)n_rb * 8);
       item0 = (int*)ctx->scratch_get(tag + ".item0", (size_t)n_rb * 2 * 4);
@@ -225,6 +241,11 @@ void MatvecOp::prepare() {
       LGP_CUDA_CHECK(cudaMemcpyAsync(nsegb, ns.data(), ns.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
       partial = (double*)ctx->scratch_get(tag + ".rowp", (size_t)n_items * 128 * 8);
       colpart = (double*)ctx->scratch_get(tag + ".colp", (size_t)std::max<long long>(rec, 1) * 64 * 8);
+      if (item_lo != 0 || item_hi != n_items) {
+        // partial records of other ranks' items stay zero in this rank's sums
+        LGP_CUDA_CHECK(cudaMemsetAsync(partial, 0, (size_t)n_items * 128 * 8, ctx->stream));
+        LGP_CUDA_CHECK(cudaMemsetAsync(colpart, 0, (size_t)std::max<long long>(rec, 1) * 64 * 8, ctx->stream));
+      }
       vpack = (double*)ctx->scratch_get(tag + ".v", (size_t)std::max(n_rows_pad, n_cols_pad) * 8);
     }
     return;
@@ -318,9 +339,12 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
       a.rowpart = partial;
       a.colpart = colpart;
       a.done = done;
+      a.item_base = item_lo;
       std::memcpy(a.kc, plan.tca.kc, sizeof a.kc);
       prof_begin();
-      launch(ctx, mod->tcsym, (unsigned)n_items, 1, 64 + 128 * plan.ts_nwg, plan.smem_tcsym, &a);
+      if (item_hi > item_lo)
+        launch(ctx, mod->tcsym, (unsigned)(item_hi - item_lo), 1, 64 + 128 * plan.ts_nwg,
+               plan.smem_tcsym, &a);
       prof_end();
       vec::tcsym_epilogue(ctx, partial, colpart, item0, nsegb, colbase, n_rows, plan.root_scale,
                           noise, noise_v, out_dev, done);
@@ -477,7 +501,28 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   op.t = t;
   op.tag = "cg.mv";
   op.allow_tc = std::getenv("LGP_CG_TC") != nullptr;  // experiment: CG on the tensor-core K1
-  op.prepare();
+  if (ctx->sharded() && t == 1 && !std::getenv("LGP_NO_RANK_SPLIT")) {
+    // try the rank-split symmetric schedule: all rows, a share of the pairs
+    op.rank_split = true;
+    op.row0 = 0;
+    op.n_rows = n;
+    op.prepare();
+    if (!op.tcsym) {  // ineligible tree: back to local rows + all-gather
+      op = MatvecOp{};
+      op.ctx = ctx;
+      op.k = k;
+      op.rows = pts;
+      op.cols = pts;
+      op.row0 = r0;
+      op.n_rows = r1 - r0;
+      op.t = t;
+      op.tag = "cg.mv";
+      op.prepare();
+    }
+  } else {
+    op.prepare();
+  }
+  const bool split = op.rank_split && op.tcsym;
 
   vec::dot_partial(ctx, B_dev, B_dev, n, t, b.part, nullptr);
   vec::dot_final(ctx, b.part, nblk, t, b.bb, nullptr);
@@ -492,8 +537,15 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
                                  ctx->stream));
   LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   for (int it = 1; it <= max_iter && !done_h; ++it) {
-    op.run(b.p, b.ap + r0 * t, noise, b.p + r0 * t, b.s.done);
-    if (ctx->sharded()) comm_allgather_inplace(ctx->comm, b.ap, (size_t)S * t, ctx->stream);
+    if (split) {
+      // this rank's pair share over all rows (noise term on rank 0 only), then
+      // the sum over ranks: one all-reduce of n doubles per iteration
+      op.run(b.p, b.ap, ctx->rank == 0 ? noise : 0.0, ctx->rank == 0 ? b.p : nullptr, b.s.done);
+      comm_allreduce_sum_inplace(ctx->comm, b.ap, (size_t)n, ctx->stream);
+    } else {
+      op.run(b.p, b.ap + r0 * t, noise, b.p + r0 * t, b.s.done);
+      if (ctx->sharded()) comm_allgather_inplace(ctx->comm, b.ap, (size_t)S * t, ctx->stream);
+    }
     vec::dot_partial(ctx, b.p, b.ap, n, t, b.part, b.s.done);
     vec::cg_fin_pap(ctx, b.part, nblk, t, b.s);
     vec::cg_update_xr(ctx, b.x, b.r, b.p, b.ap, n, t, b.s, b.part);

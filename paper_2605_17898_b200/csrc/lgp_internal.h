@@ -205,6 +205,8 @@ void comm_unique_id(uint8_t* out128);
 // in-place all-gather: buf holds world slices of `count` doubles; this
 // rank's slice is at buf + rank*count.
 void comm_allgather_inplace(Comm* c, double* buf, size_t count, cudaStream_t stream);
+// buf[0, count) <- sum over ranks, identical bits on every rank
+void comm_allreduce_sum_inplace(Comm* c, double* buf, size_t count, cudaStream_t stream);
 
 // ------------------------------------------------------ matvec engine
 // Device-resident matvec: out_rows[n_rows_local x t] for rows
@@ -225,6 +227,10 @@ struct MatvecOp {
   bool allow_tc = false;  // may use the tensor-core K1 (matvec API, Lanczos; not CG)
   bool sym = false;       // square operator on one rank: symmetric block-pair kernel
   bool tcsym = false;     // square operator, t = 1, one rank: symmetric tensor-core kernel
+  // multi-rank CG: every rank evaluates its share of the symmetric pair items
+  // over ALL rows (K1-TC-sym), the per-rank products are all-reduced
+  bool rank_split = false;
+  int item_lo = 0, item_hi = 0;  // this rank's items [lo, hi) (rank_split)
   int n_items = 0;
   int* items = nullptr;          // tcsym: [n_items][3]
   long long* colbase = nullptr;  // tcsym: [n_rb]
@@ -263,6 +269,8 @@ std::string jit_compile(const std::string& source, std::string* log_out);
 
 // ------------------------------------------------------ AOT FP64 kernels
 namespace vec {
+// dst += src (elementwise, stream-ordered; no launch accounting: comm helper)
+void add_inplace(double* dst, const double* src, int64_t n, cudaStream_t stream);
 int reduce_blocks(int64_t n, int t);
 void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int tb, int n_pass,
               double* out, const int* done);

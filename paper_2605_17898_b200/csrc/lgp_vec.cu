@@ -243,6 +243,12 @@ __global__ void k_sym_epilogue(const double* __restrict__ rowp, const double* __
   }
 }
 
+__global__ void k_add_inplace(double* __restrict__ dst, const double* __restrict__ src, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = __dadd_rn(dst[i], src[i]);
+}
+
 __global__ void k_fill(double* p, long long n, double v) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x)
@@ -829,6 +835,12 @@ void dot_partial(Context* c, const double* a, const double* b, int64_t n, int t,
 void dot_final(Context* c, const double* part, int nblk, int t, double* out, const int* done) {
   k_dot_final<<<1, 256, 0, c->stream>>>(part, nblk, t, out, done);
   LGP_LAUNCH_CHECK(c);
+}
+
+void add_inplace(double* dst, const double* src, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return;
+  k_add_inplace<<<grid_for(n), 256, 0, stream>>>(dst, src, n);
+  LGP_CUDA_CHECK(cudaGetLastError());
 }
 
 void fill(Context* c, double* p, int64_t n, double v) {
