@@ -1,7 +1,9 @@
 """World-size-2 (gloo, CPU) coverage of the multi-GPU path's host logic:
 the library's row partition, the NCCL unique-id exchange used by
-distributed.init(), and the sharded-CG schedule (local rows of K.p ->
-all-gather -> redundant FP64 updates) reproducing the unsharded reference CG."""
+distributed.init(), the sharded-CG schedule (local rows of K.p -> all-gather
+-> redundant FP64 updates) and the multi-rank symmetric schedule (a share of
+the block pairs over all rows -> all-reduce), both reproducing the unsharded
+reference CG."""
 
 import os
 import socket
@@ -68,6 +70,30 @@ def _worker(rank, world, port, q):
 
         xs, it, rr = O.cg(sharded_apply, b, 1e-10)
         res["cg"] = (xs, it, rr)
+        # 4. multi-rank symmetric schedule (engine.cpp cg_device, rank_split):
+        #    each rank evaluates a contiguous share of the block pairs (I, J >= I)
+        #    over ALL rows - K_IJ p_J into rows I and K_IJ^T p_I into rows J -
+        #    and one all-reduce (sum) yields the full product on every rank
+        B = 128
+        nb = -(-n // B)
+        pairs = [(I, J) for I in range(nb) for J in range(I, nb)]
+        lo, hi = len(pairs) * rank // world, len(pairs) * (rank + 1) // world
+
+        def split_apply(p):
+            part = np.zeros(n)
+            for I, J in pairs[lo:hi]:
+                i0, i1, j0, j1 = I * B, min(n, (I + 1) * B), J * B, min(n, (J + 1) * B)
+                k = O.gram(nodes, x[i0:i1], x[j0:j1])
+                part[i0:i1] += k @ p[j0:j1]
+                if J != I:
+                    part[j0:j1] += k.T @ p[i0:i1]
+            if rank == 0:
+                part += 0.1 * p
+            t = torch.from_numpy(part)
+            dist.all_reduce(t)
+            return t.numpy().copy()
+
+        res["cg_split"] = O.cg(split_apply, b, 1e-10)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -104,3 +130,9 @@ def test_world2_partition_id_and_sharded_cg():
     np.testing.assert_array_equal(x0, x1)
     assert it0 == it1 == ref[1]
     np.testing.assert_allclose(x0, ref[0], rtol=0, atol=1e-9 * np.abs(ref[0]).max())
+    # symmetric pair split + all-reduce: identical on both ranks, equal to the reference
+    xs0, its0, _ = out[0]["cg_split"]
+    xs1, its1, _ = out[1]["cg_split"]
+    np.testing.assert_array_equal(xs0, xs1)
+    assert its0 == its1 and abs(its0 - ref[1]) <= 1
+    np.testing.assert_allclose(xs0, ref[0], rtol=0, atol=1e-8 * np.abs(ref[0]).max())
