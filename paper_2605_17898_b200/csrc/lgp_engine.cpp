@@ -230,6 +230,8 @@ void MatvecOp::prepare() {
         item_lo = cut[ctx->rank];
         item_hi = cut[ctx->rank + 1];
       }
+      blk_lo = item_hi > item_lo ? it[3 * item_lo] : 0;
+      blk_hi = item_hi > item_lo ? it[3 * (item_hi - 1)] : -1;
       items = (int*)ctx->scratch_get(tag + ".items", it.size() * 4);
       colbase = (long long*)ctx->scratch_get(tag + ".colbase", (size_t)n_rb * 8);
       item0 = (int*)ctx->scratch_get(tag + ".item0", (size_t)n_rb * 2 * 4);
@@ -347,7 +349,7 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
                plan.smem_tcsym, &a);
       prof_end();
       vec::tcsym_epilogue(ctx, partial, colpart, item0, nsegb, colbase, n_rows, plan.root_scale,
-                          noise, noise_v, out_dev, done);
+                          noise, noise_v, out_dev, done, blk_lo, blk_hi);
       return;
     }
     vec::pack_rhs_tc(ctx, V_dev, cols->n, t, n_tiles, tb, n_pass, vtc, vscale, v_inexact, done);

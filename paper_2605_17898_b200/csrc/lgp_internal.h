@@ -231,6 +231,7 @@ struct MatvecOp {
   // over ALL rows (K1-TC-sym), the per-rank products are all-reduced
   bool rank_split = false;
   int item_lo = 0, item_hi = 0;  // this rank's items [lo, hi) (rank_split)
+  int blk_lo = 0, blk_hi = 0;    // row blocks those items cover (inclusive)
   int n_items = 0;
   int* items = nullptr;          // tcsym: [n_items][3]
   long long* colbase = nullptr;  // tcsym: [n_rb]
@@ -282,7 +283,8 @@ void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int
 // segments + column partials (I, chunk(i)) for I <= chunk(i) / 2) + noise * v_i
 void tcsym_epilogue(Context* c, const double* rowpart, const double* colpart, const int* item0,
                     const int* nseg, const long long* colbase, int64_t n, double scale,
-                    double noise, const double* noise_v, double* out, const int* done);
+                    double noise, const double* noise_v, double* out, const int* done,
+                    int blk_lo, int blk_hi);
 void epilogue(Context* c, const double* partial, int n_seg, int n_pass, int64_t rows_pad, int tb,
               int64_t n_rows, int t, double scale, double noise, const double* noise_v,
               double* out, const int* done);

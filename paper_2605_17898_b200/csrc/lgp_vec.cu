@@ -694,14 +694,16 @@ __global__ void __launch_bounds__(64 * kTsGroups)
                      const int* __restrict__ item0, const int* __restrict__ nseg,
                      const long long* __restrict__ colbase, long long n, double scale,
                      double noise, const double* __restrict__ noise_v, double* __restrict__ out,
-                     const int* done) {
+                     const int* done, int blk_lo, int blk_hi) {
   __shared__ double part[kTsGroups][64];
   if (is_done(done)) return;
   const long long c = blockIdx.x;
   const int jj = threadIdx.x & 63, g = threadIdx.x >> 6;
-  const long long last = c >> 1;
+  // only row blocks [blk_lo, blk_hi] carry records (a rank's share of the
+  // pair items in the multi-rank CG; all blocks on one rank)
+  const long long last = (c >> 1) < blk_hi ? (c >> 1) : blk_hi;
   double s = 0.0;
-  long long I2 = g;
+  long long I2 = blk_lo + g;
   for (; I2 + 3 * kTsGroups <= last; I2 += 4 * kTsGroups) {
     double v[4];
 #pragma unroll
@@ -717,7 +719,7 @@ __global__ void __launch_bounds__(64 * kTsGroups)
   const long long i = c * 64 + jj;
   if (g == 0 && i < n) {
     const int I = (int)(c >> 1), r = (int)((c & 1) * 64 + jj);
-    const int f = item0[I], m = nseg[I];
+    const int f = item0[I], m = (I >= blk_lo && I <= blk_hi) ? nseg[I] : 0;
     double t = 0.0;
     for (int k = 0; k < m; ++k) t += rowpart[(size_t)(f + k) * 128 + r];
 #pragma unroll
@@ -782,10 +784,11 @@ void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int
 
 void tcsym_epilogue(Context* c, const double* rowpart, const double* colpart, const int* item0,
                     const int* nseg, const long long* colbase, int64_t n, double scale,
-                    double noise, const double* noise_v, double* out, const int* done) {
+                    double noise, const double* noise_v, double* out, const int* done,
+                    int blk_lo, int blk_hi) {
   if (n <= 0) return;
   k_tcsym_epilogue<<<(unsigned)((n + 63) / 64), 64 * kTsGroups, 0, c->stream>>>(
-      rowpart, colpart, item0, nseg, colbase, n, scale, noise, noise_v, out, done);
+      rowpart, colpart, item0, nseg, colbase, n, scale, noise, noise_v, out, done, blk_lo, blk_hi);
   LGP_LAUNCH_CHECK(c);
 }
 
