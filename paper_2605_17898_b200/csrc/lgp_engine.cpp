@@ -533,7 +533,11 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   // host-side stop checks: every iteration for large operators, else in
   // batches (kernels after convergence early-exit on the device flag)
   const double entries = (double)n * (double)n * t;
-  const int check_every = entries > 2e8 ? 1 : 8;
+  // the host reads the device done flag every few iterations: a per-iteration
+  // round trip leaves the GPU idle between iterations (~30 us at cfg4), while
+  // iterations enqueued past convergence exit at their first instruction
+  int check_every = entries > 2e8 ? 4 : 8;
+  if (const char* e = std::getenv("LGP_CG_CHECK")) check_every = std::max(1, atoi(e));
   int done_h = 0;
   LGP_CUDA_CHECK(cudaMemcpyAsync(&done_h, b.s.done, sizeof(int), cudaMemcpyDeviceToHost,
                                  ctx->stream));
@@ -619,7 +623,11 @@ void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, doub
   vec::lz_init(ctx, Z_dev, basis, n, t, zz, s);
   const int64_t stride = (int64_t)n_alloc * t;
   const double entries = (double)n * (double)n * t;
-  const int check_every = entries > 2e8 ? 1 : 8;
+  // the host reads the device done flag every few iterations: a per-iteration
+  // round trip leaves the GPU idle between iterations (~30 us at cfg4), while
+  // iterations enqueued past convergence exit at their first instruction
+  int check_every = entries > 2e8 ? 4 : 8;
+  if (const char* e = std::getenv("LGP_CG_CHECK")) check_every = std::max(1, atoi(e));
   int done_h = 0;
   for (int j = 0; j < steps && !done_h; ++j) {
     double* q = basis + (size_t)j * stride;
