@@ -10,6 +10,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
+#include <iterator>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -116,6 +117,8 @@ Comm* comm_create(int rank, int world, const uint8_t* id128, cudaStream_t stream
   if (std::memcmp(id128, kLoopMagic, sizeof(kLoopMagic) - 1) == 0) {
     const std::string key(reinterpret_cast<const char*>(id128), 128);
     std::lock_guard<std::mutex> g(g_loop_mu);
+    for (auto it = g_loop.begin(); it != g_loop.end();)  // drop finished groups
+      it = it->second.expired() ? g_loop.erase(it) : std::next(it);
     std::shared_ptr<Loopback> lb = g_loop[key].lock();
     if (!lb) {
       lb = std::make_shared<Loopback>();
