@@ -484,6 +484,40 @@ __global__ void k_lz_multidot(const double* __restrict__ basis, long long stride
   }
 }
 
+// Same partials, one (k, c) pair per thread: block (row chunk, k group of
+// blockDim / t basis vectors); no shared-memory reduction, 8 rows in flight.
+// part[blk][k][c] = sum over the chunk's rows, in row order.
+__global__ void __launch_bounds__(256) k_lz_multidot2(const double* __restrict__ basis,
+                                                      long long stride_k, int nb,
+                                                      const double* __restrict__ w, long long n,
+                                                      int t, long long chunk, double* part,
+                                                      const int* done) {
+  if (is_done(done)) return;
+  const int kb = blockDim.x / t;
+  const int kk = threadIdx.x / t, c = threadIdx.x - kk * t;
+  const int k = blockIdx.y * kb + kk;
+  if (kk >= kb || k >= nb) return;
+  const long long r0 = (long long)blockIdx.x * chunk;
+  long long r1 = r0 + chunk;
+  if (r1 > n) r1 = n;
+  const double* __restrict__ bk = basis + (size_t)k * stride_k + c;
+  const double* __restrict__ wc = w + c;
+  double s = 0.0;
+  long long i = r0;
+  for (; i + 8 <= r1; i += 8) {
+    double bv[8], wv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      bv[u] = bk[(i + u) * t];
+      wv[u] = wc[(i + u) * t];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = fma(bv[u], wv[u], s);
+  }
+  for (; i < r1; ++i) s = fma(bk[i * t], wc[i * t], s);
+  part[((size_t)blockIdx.x * nb + k) * t + c] = s;
+}
+
 // h[e] = sum over blocks of part[blk][e], e < m = nb * t: 32 entries per block
 // (coalesced rows), 8 warps over the blocks (b = warp, warp + 8, ...), combined
 // in warp order (deterministic)
@@ -903,8 +937,14 @@ void lz_update1(Context* c, double* w, const double* q, const double* qprev, int
 void lz_multidot(Context* c, const double* basis, int64_t stride, int nb, const double* w,
                  int64_t n, int t, double* part, const int* done) {
   const int nblk = reduce_blocks(n, t);
-  k_lz_multidot<<<nblk, reduce_bd(t), 0, c->stream>>>(basis, stride, nb, w, n, t,
-                                                      chunk_rows(n, nblk), part, done);
+  if (2 * t <= 256 && !std::getenv("LGP_LZ_MULTIDOT1")) {
+    const int kb = 256 / t;
+    k_lz_multidot2<<<dim3(nblk, (nb + kb - 1) / kb), kb * t, 0, c->stream>>>(
+        basis, stride, nb, w, n, t, chunk_rows(n, nblk), part, done);
+  } else {
+    k_lz_multidot<<<nblk, reduce_bd(t), 0, c->stream>>>(basis, stride, nb, w, n, t,
+                                                        chunk_rows(n, nblk), part, done);
+  }
   LGP_LAUNCH_CHECK(c);
 }
 
