@@ -115,7 +115,13 @@ void MatvecOp::prepare() {
       tcsym = true;
     }
   }
-  if (!tcsym && allow_tc) plan = make_tc_plan(k->tree, rows->d, t, flags);
+  if (!tcsym && allow_tc) {
+    plan = make_tc_plan(k->tree, rows->d, t, flags);
+    // many Periodic features (> 24 per point) spill in the multi-RHS
+    // epilogue: the SIMT kernel is faster there (2 leaves at D = 8: 2.97 vs
+    // 3.59 ms; tools/periodic_pf_sweep.py); the t = 1 symmetric kernel still wins
+    if (plan.tc && plan.tc_pf > 24) plan.tc = false;
+  }
   if (plan.tc) {
     tb = plan.tc_n;
   } else {
