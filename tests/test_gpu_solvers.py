@@ -186,3 +186,28 @@ def test_symmetric_tensor_core_cg_dims(gpu_ctx, monkeypatch, d, expr):
     res = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
     assert abs(res.iterations - base.iterations) <= max(2, 0.03 * base.iterations)
     assert rel_l2(res.x, base.x) <= 1e-4
+
+
+@pytest.mark.parametrize("expr,d", [("(scale 1.2 (rbf 0.6))", 8),
+                                    ("(+ (scale 1.0 (rbf 0.5)) (scale 1.0 (periodic 1.0 1.0)))", 2)])
+def test_device_results_are_deterministic(gpu_ctx, expr, d):
+    """Every reduction on the device runs in a fixed order (no atomics): the
+    same inputs give bit-identical products, CG iterates and Lanczos
+    coefficients on repeated calls (tensor-core, symmetric and SIMT paths)."""
+    x, b = small_inputs(6000, d, 47)
+    k = G.parse_kernel(expr)
+    op = G.KernelOperator(k, x, 0.1)
+    V = np.random.default_rng(3).standard_normal((6000, 16))
+    m1, m2 = op(V), op(V)
+    np.testing.assert_array_equal(m1, m2)
+    v1, v2 = op(b), op(b)
+    np.testing.assert_array_equal(v1, v2)
+    r1 = G.cg_solve(op, b, G.CgConfig(rel_tolerance=1e-8))
+    r2 = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
+    assert r1.iterations == r2.iterations
+    np.testing.assert_array_equal(r1.x, r2.x)
+    z = G.probe_block(6000, 16, 0)
+    a1, b1, c1 = op.lanczos(z, 20)
+    a2, b2, c2 = op.lanczos(z, 20)
+    np.testing.assert_array_equal(a1, a2)
+    np.testing.assert_array_equal(b1, b2)
