@@ -94,6 +94,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes a few hundred ms to start: wait for its first
+            # sample so the (short) timed region is covered
+            t_wait = time.time() + 5.0
+            while not self.lines and time.time() < t_wait and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
