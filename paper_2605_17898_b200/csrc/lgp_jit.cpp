@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <atomic>
 #include <mutex>
 #include <vector>
 #include <sstream>
@@ -103,7 +104,10 @@ bool read_file(const std::string& path, std::string& out) {
 
 void write_file_atomic(const std::string& dir, const std::string& path, const std::string& data) {
   mkdir(dir.c_str(), 0755);
-  const std::string tmp = path + ".tmp" + std::to_string(getpid());
+  // unique per process AND per call: concurrent contexts in one process (host
+  // threads) may compile the same tree at the same time
+  static std::atomic<unsigned long long> seq{0};
+  const std::string tmp = path + ".tmp" + std::to_string(getpid()) + "." + std::to_string(seq++);
   {
     std::ofstream f(tmp, std::ios::binary);
     if (!f) return;

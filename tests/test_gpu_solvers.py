@@ -211,3 +211,19 @@ def test_device_results_are_deterministic(gpu_ctx, expr, d):
     a2, b2, c2 = op.lanczos(z, 20)
     np.testing.assert_array_equal(a1, a2)
     np.testing.assert_array_equal(b1, b2)
+
+
+def test_evidence_objective_batch_matches_sequential(gpu_ctx):
+    """An optimiser step's 2P + 1 evidence evaluations run concurrently (one
+    context / stream per worker thread) and give the same bits as one-by-one
+    calls on the default context."""
+    rng = np.random.default_rng(23)
+    x = rng.random((900, 3))
+    y = np.sin(2.0 * x.sum(1)) + 0.1 * rng.standard_normal(900)
+    kernel = G.parse_kernel("(scale 1.2 (rbf 0.4))")
+    obj = G.exact_evidence_objective(x, y, kernel, seed=0, workers=7)
+    p = G.flatten_model_params(kernel, 0.1)
+    qs = [p, *[p + np.eye(3)[i] * s for i in range(3) for s in (1e-4, -1e-4)]]
+    batch = obj.batch(qs)
+    seq = [obj(q) for q in qs]
+    assert batch == seq
