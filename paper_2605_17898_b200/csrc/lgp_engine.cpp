@@ -224,7 +224,7 @@ void MatvecOp::prepare() {
       item_hi = n_items;
       if (rank_split && ctx->world > 1) {
         // contiguous item ranges with (nearly) equal chunk counts per rank
-        int64_t acc = 0, next = 0;
+        int64_t acc = 0;
         int r = 0;
         std::vector<int> cut(ctx->world + 1, n_items);
         cut[0] = 0;
@@ -232,7 +232,6 @@ void MatvecOp::prepare() {
           while (r < ctx->world - 1 && acc >= (int64_t)(r + 1) * total / ctx->world) cut[++r] = q;
           acc += it[3 * q + 2] - it[3 * q + 1];
         }
-        (void)next;
         item_lo = cut[ctx->rank];
         item_hi = cut[ctx->rank + 1];
       }
