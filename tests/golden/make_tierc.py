@@ -2,6 +2,7 @@
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_tierc.py cfg2
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_tierc.py cfg4
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_tierc.py cfg3
 
 Build container only (the reference is not on the GPU box).
 
@@ -99,6 +100,34 @@ def cfg4():
     log("cfg4 done")
 
 
+def cfg3():
+    # cfg3 (RBF + Periodic, N = 50000, D = 2): one reference matvec is ~3 min
+    # here, so the pinned budgets are smaller: CG after 10 iterations, the
+    # quadratures of 4 probes after 3 Lanczos steps (~22 reference matvecs)
+    cfg = O.CONFIGS["cfg3"]
+    x, y = O.synthetic(cfg["n"], cfg["d"])
+    n = x.shape[0]
+    k = M.parse_kernel(cfg["kernel"])
+    noise = cfg["noise"]
+    apply = lambda v: M.matrix_free_matvec(k, x, noise, v, block=32)  # noqa: E731
+    it = 10
+    log("cfg3 CG", it, "iterations")
+    res = M.cg_solve(apply, y, M.CgConfig(rel_tolerance=1e-30, max_iterations=it))
+    log("cfg3 CG", res.iterations, res.final_residual)
+    steps, probes = 3, 4
+    z = O.probes(n, probes, seed=0)
+    quads = np.zeros(probes)
+    for c in range(probes):
+        quads[c] = MS._lanczos_quadrature(apply, np.ascontiguousarray(z[:, c]), steps)
+        log("cfg3 probe", c, quads[c])
+    np.savez_compressed(
+        os.path.join(HERE, "tierc_cfg3.npz"), it=res.iterations, res=res.final_residual,
+        x=res.x, steps=steps, probes=probes, quads=quads,
+        note="reference matrix_free_matvec (block 32): CG after 10 iterations, "
+             "per-probe Lanczos quadratures after 3 steps (probe seed 0)")
+    log("cfg3 done")
+
+
 if __name__ == "__main__":
     for name in sys.argv[1:]:
-        {"cfg2": cfg2, "cfg4": cfg4}[name]()
+        {"cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}[name]()

@@ -60,3 +60,27 @@ def test_tierc_cfg4_pinned_budgets(gpu_ctx):
         m = int(cnt[c])
         q = G.solvers.gauss_quadrature(al[c, :m], be[c, :m - 1])
         assert abs(q - g["quads"][c]) <= 1e-5 * abs(g["quads"][c]), (c, q, g["quads"][c])
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "tierc_cfg3.npz")),
+                    reason="tierc_cfg3 fixture not generated")
+def test_tierc_cfg3_pinned_budgets(gpu_ctx):
+    """cfg3 (RBF + Periodic, N = 50000, D = 2: the Periodic features ride next
+    to the tensor-core distance tile) through the reference's real
+    matrix_free_matvec: CG after exactly 10 iterations, the Lanczos
+    quadratures of 4 probes after 3 steps."""
+    g = golden("tierc_cfg3.npz")
+    cfg = O.CONFIGS["cfg3"]
+    x, y = O.synthetic(cfg["n"], cfg["d"])
+    op = G.KernelOperator(G.parse_kernel(cfg["kernel"]), x, cfg["noise"])
+    res = G.cg_solve(op, y, G.CgConfig(rel_tolerance=1e-30, max_iterations=int(g["it"])))
+    assert res.iterations == int(g["it"])
+    assert rel_l2(res.x, g["x"]) <= 1e-3
+    assert abs(res.final_residual - float(g["res"])) <= 1e-3 * float(g["res"])
+    steps, probes = int(g["steps"]), int(g["probes"])
+    z = G.probe_block(cfg["n"], probes, 0)
+    al, be, cnt = op.lanczos(z, steps)
+    for c in range(probes):
+        m = int(cnt[c])
+        q = G.solvers.gauss_quadrature(al[c, :m], be[c, :m - 1])
+        assert abs(q - g["quads"][c]) <= 1e-5 * abs(g["quads"][c]), (c, q, g["quads"][c])
