@@ -227,3 +227,24 @@ def test_evidence_objective_batch_matches_sequential(gpu_ctx):
     batch = obj.batch(qs)
     seq = [obj(q) for q in qs]
     assert batch == seq
+
+
+@pytest.mark.parametrize("seed,n,d", [(0, 300, 2), (1, 1000, 2), (2, 3000, 8)])
+def test_cg_gram_operators_match_cholesky(gpu_ctx, seed, n, d):
+    """Reference test_solvers.py:133-147 on the device operator: CG at tol 1e-11
+    against an FP64 Cholesky solve of the same Gram. The reference's 1e-8
+    bar is for FP64 entries; with FP32 entries the solutions agree to
+    ~1e-6 relative (3e-6 absolute measured), bar 1e-5 relative."""
+    import scipy.linalg
+
+    rng = np.random.default_rng(seed)
+    x = rng.random((n, d))
+    y = rng.standard_normal(n)
+    k = G.Scale(1.3, G.RBF(0.3))
+    gram = O.gram(O.parse_tree(G.format_kernel(k)), x, x, same=True)
+    gram.flat[:: n + 1] += 1.0
+    want = scipy.linalg.cho_solve(scipy.linalg.cho_factor(gram), y)
+    res = G.cg_solve(G.KernelOperator(k, x, 1.0), y,
+                     G.CgConfig(rel_tolerance=1e-11, max_iterations=5 * n))
+    assert rel_l2(res.x, want) <= 1e-5
+    assert np.max(np.abs(res.x - want)) <= 3e-5
