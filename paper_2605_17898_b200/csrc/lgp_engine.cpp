@@ -507,7 +507,15 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   op.n_rows = r1 - r0;
   op.t = t;
   op.tag = "cg.mv";
-  op.allow_tc = std::getenv("LGP_CG_TC") != nullptr;  // experiment: CG on the tensor-core K1
+  // t = 1 (the alpha solve): exactly symmetric kernels only (K1-TC-sym /
+  // SIMT), CG counts its iterations. Multi-RHS CG (predictive variance, t = T
+  // test points): the tensor-core K1 - its rounding-level asymmetry costs
+  // iterations (~1.3x) but each costs 4.5x less than the SIMT kernel's t/16
+  // passes (cfg4, T = 200: 47 vs 210 ms); LGP_CG_TC=0/1 overrides.
+  if (const char* e = std::getenv("LGP_CG_TC"))
+    op.allow_tc = atoi(e) != 0;
+  else
+    op.allow_tc = t >= 8;
   if (ctx->sharded() && t == 1 && !std::getenv("LGP_NO_RANK_SPLIT")) {
     // try the rank-split symmetric schedule: all rows, a share of the pairs
     op.rank_split = true;
