@@ -75,8 +75,9 @@ def test_tierc_cfg3_pinned_budgets(gpu_ctx):
     op = G.KernelOperator(G.parse_kernel(cfg["kernel"]), x, cfg["noise"])
     res = G.cg_solve(op, y, G.CgConfig(rel_tolerance=1e-30, max_iterations=int(g["it"])))
     assert res.iterations == int(g["it"])
-    assert rel_l2(res.x, g["x"]) <= 1e-3
-    assert abs(res.final_residual - float(g["res"])) <= 1e-3 * float(g["res"])
+    # measured 3e-7 / 1.4e-8 / <= 2.7e-7 (tools/tierc3_check.py)
+    assert rel_l2(res.x, g["x"]) <= 1e-5
+    assert abs(res.final_residual - float(g["res"])) <= 1e-5 * float(g["res"])
     steps, probes = int(g["steps"]), int(g["probes"])
     z = G.probe_block(cfg["n"], probes, 0)
     al, be, cnt = op.lanczos(z, steps)
