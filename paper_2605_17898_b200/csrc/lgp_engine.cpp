@@ -106,8 +106,17 @@ void MatvecOp::prepare() {
   // column partials: one 64-column record per (row block, chunk) pair, n^2/8192
   // records of 512 B - bounded (N <= ~1.1M) so they fit comfortably in HBM
   const double tcsym_bytes = (double)rows->n * (double)rows->n / 8192.0 * 512.0;
+  // partial-record budget: 16 GB, or up to 40 % of the free HBM (N <= ~1.1M
+  // on a 180 GB B200; the epilogue reads the records once per matvec, ~4 % of
+  // the kernel's time at that size)
+  double tcsym_budget = kSymPartialBudget;
+  if (t == 1 && rows == cols && tcsym_bytes > tcsym_budget) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+      tcsym_budget = std::max(tcsym_budget, 0.4 * (double)free_b);
+  }
   if (t == 1 && rows == cols && (!ctx->sharded() || rank_split) && row0 == 0 && n_rows == rows->n &&
-      tcsym_bytes <= kSymPartialBudget &&
+      tcsym_bytes <= tcsym_budget &&
       !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && !std::getenv("LGP_NO_TCSYM")) {
     Plan p = make_tc_plan(k->tree, rows->d, 16, flags);
     if (p.tc && !p.tc_pair) {
