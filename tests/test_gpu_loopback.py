@@ -91,3 +91,30 @@ def test_loopback_ranks_match_one_rank(gpu_ctx, world):
         q = G.solvers.gauss_quadrature(al[c, :m], be[c, :m - 1])
         q1 = G.solvers.gauss_quadrature(ref[4][c, :m], ref[6][c, :m - 1])
         assert abs(q - q1) <= 1e-5 * abs(q1), (c, q, q1)  # 2.7e-7 seen
+
+
+def test_loopback_more_ranks_than_work(gpu_ctx):
+    """world 4 on a 300-point operator: some ranks own no pair items of the
+    symmetric CG (empty launch, no records) and the row slices are tiny; every
+    rank still ends with the one-rank solution."""
+    rng = np.random.default_rng(9)
+    n, d = 300, 5
+    x = rng.random((n, d))
+    b = rng.standard_normal(n)
+    k = G.parse_kernel("(scale 1.3 (rbf 0.7))")
+
+    def fn(ctx, r):
+        op = G.KernelOperator(k, x, 0.1, ctx=ctx)
+        xs, it, res = op.cg(b, 1e-8, None)
+        return xs.copy(), int(it[0]), op._matvec(np.ascontiguousarray(
+            np.random.default_rng(2).standard_normal((n, 9)))).copy()
+
+    outs = run_ranks(4, fn)
+    ref = run_ranks(1, fn)[0]
+    for r in range(4):
+        np.testing.assert_array_equal(outs[r][0], outs[0][0])
+        assert outs[r][1] == outs[0][1]
+        np.testing.assert_array_equal(outs[r][2], outs[0][2])
+    assert abs(outs[0][1] - ref[1]) <= 2
+    assert rel_l2(outs[0][0], ref[0]) <= 1e-6
+    assert rel_l2(outs[0][2], ref[2]) <= 1e-6
