@@ -161,24 +161,12 @@ def stdout_to_stderr():
         os.close(saved)
 
 
-def dist_setup(world):
-    if world <= 1:
-        return None
-    import torch.distributed as dist
-
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    dist.init_process_group("gloo")
-    return dist
-
-
-def max_over_ranks(dist, value):
-    if dist is None:
+def max_over_ranks(ctx, value):
+    """Max of a host value over the ranks (the library's NCCL all-reduce; no
+    torch.distributed). Identity at one rank."""
+    if ctx is None or ctx.world == 1:
         return value
-    import torch
-
-    t = torch.tensor([float(value)], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return ctx.allreduce_max([value])[0]
 
 
 def cpu_baseline(cfg, x, seconds=12.0):
@@ -277,13 +265,15 @@ def run_ours(args, rank, world):
     from paper_2605_17898_b200 import _lib, distributed
     from oracle import gp_oracle as O  # input recipe + CPU baseline only
 
-    dist = dist_setup(world)
     # rank 0 prints exactly one JSON line on stdout: NCCL's own log lines
-    # ("NCCL version ...") go to stderr
+    # (communicator set-up with nranks / transports at INFO) go to stderr
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     with stdout_to_stderr():
         ctx = distributed.init(force_comm=args.sharded) if (world > 1 or args.sharded) \
             else _lib.default_context()
+    dist = ctx if world > 1 else None
     lib = _lib.lib()
     cfg = dict(O.CONFIGS[args.config])
     n, d, t = cfg["n"], cfg["d"], cfg["t"]
@@ -475,11 +465,35 @@ def main():
                          "(exercises the multi-GPU path on one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    launched = "WORLD_SIZE" in os.environ
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if launched and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks",
+              file=sys.stderr)
+        return 2
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        # the reference is a CPU algorithm: rank 0 alone runs it (other ranks exit 0)
+        return run_reference(args, rank, args.gpus)
+    if not launched and args.gpus > 1:
+        return self_launch(args)
     return run_ours(args, rank, world)
+
+
+def self_launch(args):
+    """`bench.py --gpus N` without a launcher: start N ranks (one process per
+    GPU) ourselves, sharing an NCCL id made here (no torch.distributed)."""
+    from paper_2605_17898_b200 import _lib, distributed
+
+    have = _lib.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+              file=sys.stderr)
+        return 2
+    return distributed.launch([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                              args.gpus)
 
 
 if __name__ == "__main__":

@@ -99,6 +99,11 @@ int lgp_comm_unique_id(uint8_t* out128);
  * threads, one context each, same GPU) a loopback group with host-mediated
  * gathers (tests/test_gpu_loopback.py). */
 int lgp_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, lgp_ctx** out);
+/* Element-wise max over the context's ranks of count HOST doubles, in place
+ * (NCCL all-reduce on the context's communicator; synchronous). A context
+ * without a communicator leaves vals unchanged. Used for max-over-ranks
+ * timings and as a barrier (count = 1). */
+int lgp_comm_allreduce_max(lgp_ctx* ctx, double* vals, int32_t count);
 int lgp_ctx_destroy(lgp_ctx* ctx);
 int lgp_ctx_sync(lgp_ctx* ctx);
 /* number of kernels this library has launched on the context (for bench) */

@@ -49,6 +49,7 @@ _SIGS = {
     "lgp_partition": ([C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
                       C.c_int),
     "lgp_comm_unique_id": ([C.c_char_p], C.c_int),
+    "lgp_comm_allreduce_max": ([_P, C.POINTER(C.c_double), C.c_int32], C.c_int),
     "lgp_ctx_create": ([C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_P)], C.c_int),
     "lgp_ctx_destroy": ([_P], C.c_int),
     "lgp_ctx_sync": ([_P], C.c_int),
@@ -127,6 +128,13 @@ def check(status):
     raise MiniGpError(f"lightgp error {status}: {msg}")
 
 
+def device_count():
+    """Visible CUDA devices (0 without a GPU or driver)."""
+    n = C.c_int()
+    check(lib().lgp_device_count(C.byref(n)))
+    return n.value
+
+
 def dptr(a):
     return a.ctypes.data_as(_D)
 
@@ -185,6 +193,17 @@ class Context:
         ms = C.c_float()
         check(lib().lgp_timer_stop(self.handle, C.byref(ms)))
         return ms.value
+
+    def allreduce_max(self, values):
+        """Element-wise max over the context's ranks (library NCCL all-reduce);
+        returns a list of floats. Identity without a communicator."""
+        vals = (C.c_double * len(values))(*[float(v) for v in values])
+        check(lib().lgp_comm_allreduce_max(self.handle, vals, len(values)))
+        return list(vals)
+
+    def barrier(self):
+        """All ranks of the context reach this point (one tiny all-reduce)."""
+        self.allreduce_max([0.0])
 
     def flush_l2(self, nbytes=256 << 20):
         check(lib().lgp_flush_l2(self.handle, nbytes))

@@ -152,6 +152,16 @@ int lgp_comm_unique_id(uint8_t* out128) {
   API_END
 }
 
+int lgp_comm_allreduce_max(lgp_ctx* ctx, double* vals, int32_t count) {
+  API_BEGIN
+  require(ctx != nullptr && (vals != nullptr || count == 0) && count >= 0, LGP_E_ARG,
+          "bad all-reduce request");
+  std::lock_guard<std::recursive_mutex> g(ctx->mu);
+  ctx->activate();
+  if (ctx->comm) comm_allreduce_max_host(ctx->comm, vals, count, ctx->stream);
+  API_END
+}
+
 int lgp_ctx_create(int device, int rank, int world, const uint8_t* nccl_id, lgp_ctx** out) {
   API_BEGIN
   require(out != nullptr, LGP_E_ARG, "out is null");

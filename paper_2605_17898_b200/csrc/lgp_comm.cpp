@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
@@ -82,6 +83,7 @@ struct Loopback {
   std::vector<double*> bufs;
   std::vector<double*> tmp;  // per-rank sum buffers (all-reduce)
   std::vector<size_t> tmp_n;
+  std::vector<double*> hvals;  // per-rank host values (max all-reduce)
   void barrier() {
     std::unique_lock<std::mutex> l(mu);
     const long g = gen;
@@ -126,6 +128,7 @@ Comm* comm_create(int rank, int world, const uint8_t* id128, cudaStream_t stream
       lb->bufs.assign(world, nullptr);
       lb->tmp.assign(world, nullptr);
       lb->tmp_n.assign(world, 0);
+      lb->hvals.assign(world, nullptr);
       g_loop[key] = lb;
     }
     if (lb->world != world) throw Error(LGP_E_ARG, "loopback group world size mismatch");
@@ -209,6 +212,31 @@ void comm_allreduce_sum_inplace(Comm* c, double* buf, size_t count, cudaStream_t
     return;
   }
   check(api().all_reduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, stream), "ncclAllReduce");
+}
+
+void comm_allreduce_max_host(Comm* c, double* vals, int count, cudaStream_t stream) {
+  if (count <= 0) return;
+  if (c->loop) {
+    Loopback& lb = *c->loop;
+    std::vector<double> m(vals, vals + count);
+    {
+      std::lock_guard<std::mutex> g(lb.mu);
+      lb.hvals[c->rank] = vals;
+    }
+    lb.barrier();
+    for (int q = 0; q < c->world; ++q)
+      for (int i = 0; i < count; ++i) m[i] = std::max(m[i], lb.hvals[q][i]);
+    lb.barrier();  // every rank has read every other rank's values
+    std::memcpy(vals, m.data(), (size_t)count * sizeof(double));
+    return;
+  }
+  double* d = nullptr;
+  LGP_CUDA_CHECK(cudaMallocAsync(&d, (size_t)count * sizeof(double), stream));
+  LGP_CUDA_CHECK(cudaMemcpyAsync(d, vals, (size_t)count * sizeof(double), cudaMemcpyHostToDevice, stream));
+  check(api().all_reduce(d, d, (size_t)count, ncclFloat64, ncclMax, c->comm, stream), "ncclAllReduce(max)");
+  LGP_CUDA_CHECK(cudaMemcpyAsync(vals, d, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  LGP_CUDA_CHECK(cudaFreeAsync(d, stream));
+  LGP_CUDA_CHECK(cudaStreamSynchronize(stream));
 }
 
 }  // namespace lgp

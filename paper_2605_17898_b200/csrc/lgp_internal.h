@@ -207,6 +207,8 @@ void comm_unique_id(uint8_t* out128);
 void comm_allgather_inplace(Comm* c, double* buf, size_t count, cudaStream_t stream);
 // buf[0, count) <- sum over ranks, identical bits on every rank
 void comm_allreduce_sum_inplace(Comm* c, double* buf, size_t count, cudaStream_t stream);
+// element-wise max over ranks of `count` HOST doubles (timing / barriers; synchronous)
+void comm_allreduce_max_host(Comm* c, double* vals, int count, cudaStream_t stream);
 
 // ------------------------------------------------------ matvec engine
 // Device-resident matvec: out_rows[n_rows_local x t] for rows

@@ -3,6 +3,7 @@
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_tierc.py cfg2
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_tierc.py cfg4
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_tierc.py cfg3
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_tierc.py n50k_rbf n50k_m32
 
 Build container only (the reference is not on the GPU box).
 
@@ -16,6 +17,15 @@ tierc_cfg4.npz     cfg4 in full (N = 100000, RBF, D = 8) through the reference's
                    real matrix_free_matvec (block = 32, the fit's block): CG after
                    exactly 20 iterations, and the SLQ quadratures of 16 probes
                    after 5 Lanczos steps (equal, pinned budgets; ~1.5 h of CPU).
+tierc_n50k_rbf.npz / tierc_n50k_m32.npz
+                   the cfg4 kernel (RBF 0.5, D = 8) and the cfg5 kernel (Matern-3/2
+                   0.5, D = 8) at N = 50000 (the largest N whose FP64 Gram, 20 GB,
+                   fits this container): the reference's own cg_solve (tol 1e-8) /
+                   slq_logdet (16 probes x 50 steps) / mean / LML on the dense
+                   replay operator built slab by slab from the reference's own
+                   Kernel._gram (the entries matrix_free_matvec uses,
+                   solvers.py:79-80), plus the exact (Cholesky) latent variance at
+                   200 test points.
 """
 
 from __future__ import annotations
@@ -128,6 +138,45 @@ def cfg3():
     log("cfg3 done")
 
 
+def n50k(tag):
+    # SURVEY.md §8c tier C: "check the same kernel/D/t at a reduced N where the
+    # dense replay fits (N <= 50k)"
+    kern = {"rbf": O.CONFIGS["cfg4"]["kernel"], "m32": O.CONFIGS["cfg5"]["kernel"]}[tag]
+    n, d, noise = 50000, 8, 0.1
+    x, y = O.synthetic(n, d)
+    k = M.parse_kernel(kern)
+    log(tag, "gram (slabs of the reference's _gram)")
+    gram_y = np.empty((n, n))
+    for i0 in range(0, n, 2048):
+        i1 = min(n, i0 + 2048)
+        gram_y[i0:i1] = k._gram(x[i0:i1], x)
+    gram_y.flat[:: n + 1] += noise
+    apply = lambda v: gram_y @ v  # noqa: E731
+    fit_cfg = M.CgConfig(rel_tolerance=1e-8)  # models.py FIT_CG_TOLERANCE
+    log(tag, "CG")
+    res = M.cg_solve(apply, y, fit_cfg)
+    log(tag, "CG", res.iterations, res.final_residual)
+    ld = M.slq_logdet(apply, n, fit_cfg, seed=0)
+    quad = float(y @ res.x)
+    lml = -0.5 * (quad + ld + n * np.log(2 * np.pi))
+    log(tag, "SLQ logdet", ld, "LML", lml)
+    xs = np.random.default_rng(9).random((200, d))
+    kstar = M.kernel_eval(k, x, xs)
+    mean = kstar.T @ res.x
+    log(tag, "Cholesky")
+    # the Gram is symmetric: its transpose view is Fortran-ordered, factor in place
+    c = scipy.linalg.cho_factor(gram_y.T, lower=True, overwrite_a=True, check_finite=False)
+    half = scipy.linalg.solve_triangular(c[0], kstar, lower=True, check_finite=False)
+    var = np.maximum(M.kernel_diag(k, xs) - np.einsum("ij,ij->j", half, half), 0.0)
+    np.savez_compressed(
+        os.path.join(HERE, f"tierc_n50k_{tag}.npz"), kernel=kern, n=n, d=d, noise=noise,
+        it=res.iterations, res=res.final_residual, alpha=res.x, logdet=ld, lml=lml, mean=mean,
+        var=var, note="reference cg_solve/slq_logdet on the dense replay operator (slabs of "
+                      "Kernel._gram); var by Cholesky")
+    log(tag, "done")
+
+
 if __name__ == "__main__":
     for name in sys.argv[1:]:
-        {"cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}[name]()
+        {"cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4,
+         "n50k_rbf": lambda: n50k("rbf"), "n50k_m32": lambda: n50k("m32")}[name]()

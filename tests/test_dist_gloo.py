@@ -1,6 +1,6 @@
 """World-size-2 (gloo, CPU) coverage of the multi-GPU path's host logic:
 the library's row partition, the NCCL unique-id exchange used by
-distributed.init(), the sharded-CG schedule (local rows of K.p -> all-gather
+distributed.init() (rendezvous file, no torch.distributed), the sharded-CG schedule (local rows of K.p -> all-gather
 -> redundant FP64 updates) and the multi-rank symmetric schedule (a share of
 the block pairs over all rows -> all-reduce), both reproducing the unsharded
 reference CG."""
@@ -22,7 +22,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, rdzv):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -30,28 +30,26 @@ def _worker(rank, world, port, q):
         import sys
 
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-        import ctypes as C
-
         import torch
         from oracle import gp_oracle as O
-        from paper_2605_17898_b200 import _lib, distributed
+        from paper_2605_17898_b200 import distributed
 
         res = {}
         # 1. partition from the C ABI
         n = 1001
         r0, r1 = distributed.partition(n, world, rank)
         res["part"] = (r0, r1)
-        # 2. NCCL id exchange (what distributed.init does before lgp_ctx_create)
-        obj = [None]
-        if rank == 0:
-            buf = C.create_string_buffer(128)
-            try:
-                _lib.check(_lib.lib().lgp_comm_unique_id(buf))
-                obj[0] = buf.raw
-            except Exception as exc:  # NCCL not loadable here
-                obj[0] = f"ERR {exc}".encode()
-        dist.broadcast_object_list(obj, src=0)
-        res["id"] = obj[0]
+        # 2. NCCL id exchange of distributed.init (rendezvous file, no torch)
+        os.environ["LGP_RDZV_FILE"] = os.path.join(rdzv, "nccl-id")
+        os.environ["RANK"], os.environ["WORLD_SIZE"] = str(rank), str(world)
+        try:
+            ident, owned = distributed.exchange_id(rank, world)
+        except Exception as exc:  # NCCL not loadable here
+            ident, owned = f"ERR {exc}".encode(), None
+        dist.barrier()  # (the library's ncclCommInitRank is this barrier on a GPU box)
+        if owned:
+            os.unlink(owned)
+        res["id"] = ident
         # 3. sharded CG schedule on the oracle
         rng = np.random.default_rng(3)
         x = rng.random((n, 3))
@@ -99,12 +97,12 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_world2_partition_id_and_sharded_cg():
+def test_world2_partition_id_and_sharded_cg(tmp_path):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, str(tmp_path))) for r in range(world)]
     for p in procs:
         p.start()
     out = dict(q.get(timeout=600) for _ in range(world))
