@@ -80,21 +80,23 @@ struct LgpTcArgs {
 
 // Symmetric tensor-core K1 for the square operator with one RHS (the CG
 // matvec): every unordered pair (i, j) is evaluated once, in the tile of row
-// block min and column chunk max, and feeds out_i and out_j in FP64.
+// block min and column chunk max, and feeds out_i and out_j in FP64. Work
+// item = rectangle of row blocks [Ia, Ib) x 64-column chunks [ca, cb), at
+// most R x 2R.
 struct LgpTcSymArgs {
   const float* a1;            // row operand tiles (FP16 hi/lo features) [n_rb][128 x KD]
   const float* b1;            // column operand tiles [n_tiles][64 x KD]
   const double* v;            // RHS, zero-padded to the column padding (t = 1)
   const float* r32;           // FP32 row features [n_rows_pad][FW] (Periodic trees; else null)
   const float* c32;           // FP32 column features [n_cols_pad][FW] (Periodic trees; else null)
-  const int* items;           // [n_items][3]: row block I, chunk range [c0, c1)
-  const long long* colbase;   // [n_rb]: first column-partial record of row block I
-  double* rowpart;            // [n_items][128]
-  double* colpart;            // [records][64]: record (I, c) at colbase[I] + c - 2I
+  const int* items;           // [n_items][6]: (Ia, Ib, ca, cb, first row record, first chunk record)
+  double* rowpart;            // [row records of the launched items][128]
+  double* colpart;            // [chunk records of the launched items][64]
   const int* done;            // optional early-exit flag
-  unsigned long long* trace;  // LGP_TC_TRACE builds only
   int item_base;              // first work item of this launch (multi-rank CG: the rank's share)
-  int pad_;
+  int R;                      // max row blocks per item (column accumulators: 2R x 64)
+  int n_rb;                   // row blocks (128 rows)
+  int n_tiles;                // 64-column chunks
   float kc[LGP_MAX_KC];
 };
 #endif

@@ -8,6 +8,8 @@
 // vectors. All ranks hold bit-identical state, the host loop's stop decision
 // is identical on every rank, and no scalar all-reduce is needed.
 #include <algorithm>
+#include <functional>
+#include <vector>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -74,6 +76,65 @@ template <class T>
 T ceil_div(T a, T b) {
   return (a + b - 1) / b;
 }
+// pairs (I, c) with c >= 2I of a rectangle of the (row block, chunk) grid
+int64_t ts_pairs(int Ia, int Ib, int ca, int cb) {
+  int64_t p = 0;
+  for (int I = Ia; I < Ib; ++I) p += std::max(0, cb - std::max(ca, 2 * I));
+  return p;
+}
+// list-scheduling model: items dispatched in order onto the free-earliest SM;
+// cost ~ pairs + a row-switch and an item overhead (in pair units)
+double ts_makespan(const std::vector<TsRect>& v, int slots) {
+  std::vector<double> sm(std::max(1, slots), 0.0);
+  std::make_heap(sm.begin(), sm.end(), std::greater<double>());
+  for (const TsRect& r : v) {
+    std::pop_heap(sm.begin(), sm.end(), std::greater<double>());
+    sm.back() += (double)r.pairs + 1.0 * (r.Ib - r.Ia) + 4.0;
+    std::push_heap(sm.begin(), sm.end(), std::greater<double>());
+  }
+  return *std::max_element(sm.begin(), sm.end());
+}
+}  // namespace
+
+std::vector<TsRect> ts_items(int n_rb, int n_tiles, int R, int slots) {
+  std::vector<TsRect> base;
+  const int nG = (int)ceil_div<int64_t>(n_rb, R);
+  auto add = [&](std::vector<TsRect>& v, int Ia, int Ib, int ca, int cb) {
+    Ib = std::min(Ib, n_rb);
+    cb = std::min(cb, n_tiles);
+    if (Ia >= Ib || ca >= cb) return;
+    const int64_t p = ts_pairs(Ia, Ib, ca, cb);
+    if (p > 0) v.push_back(TsRect{Ia, Ib, ca, cb, p});
+  };
+  for (int d = 1; d < nG; ++d)
+    for (int gi = 0; gi + d < nG; ++gi) add(base, gi * R, (gi + 1) * R, 2 * (gi + d) * R, 2 * (gi + d + 1) * R);
+  for (int gi = 0; gi < nG; ++gi) add(base, gi * R, (gi + 1) * R, 2 * gi * R, 2 * (gi + 1) * R);
+  // quarters for the items that start within the last two waves of work
+  int64_t total = 0, big = 1;
+  for (const TsRect& r : base) {
+    total += r.pairs;
+    big = std::max(big, r.pairs);
+  }
+  const int64_t tail = 2 * (int64_t)std::max(1, slots) * big;
+  std::vector<TsRect> out;
+  int64_t acc = 0;
+  for (const TsRect& r : base) {
+    if (R > 1 && total - acc <= tail) {
+      const int Im = (r.Ia + r.Ib + 1) / 2, cm = (r.ca + r.cb + 1) / 2;
+      add(out, r.Ia, Im, r.ca, cm);
+      add(out, r.Ia, Im, cm, r.cb);
+      add(out, Im, r.Ib, r.ca, cm);
+      add(out, Im, r.Ib, cm, r.cb);
+    } else {
+      out.push_back(r);
+    }
+    acc += r.pairs;
+  }
+  std::stable_sort(out.begin(), out.end(), [](const TsRect& x, const TsRect& y) { return x.pairs > y.pairs; });
+  return out;
+}
+
+namespace {
 void launch(Context* ctx, CUfunction f, unsigned gx, unsigned gy, unsigned bx, size_t smem,
             void* args) {
   void* params[] = {args};
@@ -98,25 +159,13 @@ void MatvecOp::prepare() {
       flags |= LGP_DIST_DIRECT;
     }
   }
-  // the CG matvec (square operator, one RHS, one rank): symmetric tensor-core
-  // kernel, each unordered pair evaluated once, FP64 contraction with the
-  // exact p - exactly symmetric, so CG iteration counts match the SIMT kernel;
-  // 3.35 vs 4.21 ms on cfg4 (profiles/r01_tcsym.txt). LGP_NO_TCSYM disables.
+  // the CG matvec (square operator, one RHS): symmetric tensor-core kernel,
+  // each unordered pair evaluated once, FP64 contraction with the exact p -
+  // exactly symmetric, so CG iteration counts match the SIMT kernel. Its
+  // scratch is O(N) (super-tiles, see prepare below), so the choice depends on
+  // the tree and flags only: identical on every rank of a multi-rank CG.
   tcsym = false;
-  // column partials: one 64-column record per (row block, chunk) pair, n^2/8192
-  // records of 512 B - bounded (N <= ~1.1M) so they fit comfortably in HBM
-  const double tcsym_bytes = (double)rows->n * (double)rows->n / 8192.0 * 512.0;
-  // partial-record budget: 16 GB, or up to 40 % of the free HBM (N <= ~1.1M
-  // on a 180 GB B200; the epilogue reads the records once per matvec, ~4 % of
-  // the kernel's time at that size)
-  double tcsym_budget = kSymPartialBudget;
-  if (t == 1 && rows == cols && tcsym_bytes > tcsym_budget) {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
-      tcsym_budget = std::max(tcsym_budget, 0.4 * (double)free_b);
-  }
   if (t == 1 && rows == cols && (!ctx->sharded() || rank_split) && row0 == 0 && n_rows == rows->n &&
-      tcsym_bytes <= tcsym_budget &&
       !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && !std::getenv("LGP_NO_TCSYM")) {
     Plan p = make_tc_plan(k->tree, rows->d, 16, flags);
     if (p.tc && !p.tc_pair) {
@@ -166,7 +215,7 @@ void MatvecOp::prepare() {
   tiles_per_seg = ceil_div(n_tiles, best);
   n_seg = ceil_div(n_tiles, tiles_per_seg);
 
-  partial = (double*)ctx->scratch_get(tag + ".part", (size_t)n_seg * n_pass * n_rows_pad * tb * 8);
+  if (!tcsym) partial = (double*)ctx->scratch_get(tag + ".part", (size_t)n_seg * n_pass * n_rows_pad * tb * 8);
   if (plan.tc) {
     // operands pre-tiled in the UMMA canonical layout, FP16 hi/lo split
     fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * plan.tc_kd * 2);
@@ -208,60 +257,96 @@ void MatvecOp::prepare() {
                                    128, 1, 1, 0, (CUstream)ctx->stream, p2, nullptr));
     ++ctx->launches;
     if (tcsym) {
-      // work items: row block I x a segment of its column chunks [2I, n_tiles);
-      // column partial records (I, c) laid out block after block
-      int64_t total = 0;
-      for (int I = 0; I < n_rb; ++I) total += std::max(0, n_tiles - 2 * I);
-      const int S = (int)std::max<int64_t>(8, ceil_div<int64_t>(total, (int64_t)ctx->sm_count * 16));
-      std::vector<int> it, f0(n_rb), ns(n_rb);
-      std::vector<long long> cb(n_rb);
-      long long rec = 0;
-      for (int I = 0; I < n_rb; ++I) {
-        const int cs = 2 * I, m = std::max(0, n_tiles - cs);
-        cb[I] = rec;
-        f0[I] = (int)(it.size() / 3);
-        ns[I] = ceil_div(m, S);
-        for (int g = 0; g < ns[I]; ++g) {
-          it.push_back(I);
-          it.push_back(cs + g * S);
-          it.push_back(std::min(cs + (g + 1) * S, n_tiles));
+      // work items: rectangles of the (row block, chunk) triangle c >= 2I -
+      // R x 2R super-tiles (full ones first, the diagonal ones after), the
+      // ones dispatched in the last two waves split into quarters; R picked
+      // by a list-scheduling model of the items on the SMs (one CTA per SM)
+      // so the items fill whole waves while the scratch (R x 128 + 2R x 64
+      // doubles per item) stays O(N)
+      int R = 1;
+      std::vector<TsRect> rects;
+      {
+        const int cands[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64};
+        double best = 1e300;
+        int forced = 0;
+        if (const char* e = std::getenv("LGP_TS_R")) forced = std::max(1, std::min(kTsRMax, atoi(e)));
+        for (int Rc : cands) {
+          if (Rc > kTsRMax) break;
+          if (forced && Rc != forced) continue;
+          const int64_t nG = ceil_div<int64_t>(n_rb, Rc);
+          if (nG * (nG + 1) / 2 > 2000000) continue;
+          std::vector<TsRect> rc = ts_items(n_rb, n_tiles, Rc, ctx->sm_count);
+          const double span = ts_makespan(rc, ctx->sm_count);
+          if (span < best * 0.995) {  // near-ties: the larger R (less scratch)
+            best = span;
+            R = Rc;
+            rects.swap(rc);
+          } else if (span <= best * 1.005) {
+            R = Rc;
+            rects.swap(rc);
+          }
         }
-        rec += m;
+        if (forced) R = forced;
       }
-      n_items = (int)(it.size() / 3);
+      n_items = (int)rects.size();
+      ts_R = R;
       item_lo = 0;
       item_hi = n_items;
       if (rank_split && ctx->world > 1) {
-        // contiguous item ranges with (nearly) equal chunk counts per rank
+        // contiguous item ranges with (nearly) equal pair counts per rank
+        int64_t total = 0;
+        for (const TsRect& r : rects) total += r.pairs;
         int64_t acc = 0;
         int r = 0;
         std::vector<int> cut(ctx->world + 1, n_items);
         cut[0] = 0;
         for (int q = 0; q < n_items; ++q) {
           while (r < ctx->world - 1 && acc >= (int64_t)(r + 1) * total / ctx->world) cut[++r] = q;
-          acc += it[3 * q + 2] - it[3 * q + 1];
+          acc += rects[q].pairs;
         }
         item_lo = cut[ctx->rank];
         item_hi = cut[ctx->rank + 1];
       }
-      blk_lo = item_hi > item_lo ? it[3 * item_lo] : 0;
-      blk_hi = item_hi > item_lo ? it[3 * (item_hi - 1)] : -1;
+      // item table (Ia, Ib, ca, cb, first row record, first chunk record) +
+      // the records each row block / chunk sums (this rank's items, in item
+      // order: the epilogue's fixed summation order)
+      std::vector<int> it((size_t)n_items * 6);
+      std::vector<std::vector<int>> rl(n_rb), cl(n_tiles);
+      int nrr = 0, ncr = 0;
+      for (int q = 0; q < n_items; ++q) {
+        const TsRect& r = rects[q];
+        it[6 * q] = r.Ia;
+        it[6 * q + 1] = r.Ib;
+        it[6 * q + 2] = r.ca;
+        it[6 * q + 3] = r.cb;
+        it[6 * q + 4] = nrr;
+        it[6 * q + 5] = ncr;
+        if (q < item_lo || q >= item_hi) continue;
+        for (int I = r.Ia; I < r.Ib; ++I) rl[I].push_back(nrr++);
+        for (int c = r.ca; c < r.cb; ++c) cl[c].push_back(ncr++);
+      }
+      std::vector<int> idx;
+      idx.reserve((size_t)n_rb + n_tiles + 2 + nrr + ncr);
+      idx.push_back(0);
+      for (int I = 0; I < n_rb; ++I) idx.push_back(idx.back() + (int)rl[I].size());
+      idx.push_back(0);
+      for (int c = 0; c < n_tiles; ++c) idx.push_back(idx.back() + (int)cl[c].size());
+      for (int I = 0; I < n_rb; ++I) idx.insert(idx.end(), rl[I].begin(), rl[I].end());
+      for (int c = 0; c < n_tiles; ++c) idx.insert(idx.end(), cl[c].begin(), cl[c].end());
       items = (int*)ctx->scratch_get(tag + ".items", it.size() * 4);
-      colbase = (long long*)ctx->scratch_get(tag + ".colbase", (size_t)n_rb * 8);
-      item0 = (int*)ctx->scratch_get(tag + ".item0", (size_t)n_rb * 2 * 4);
-      nsegb = item0 + n_rb;
+      recs = (int*)ctx->scratch_get(tag + ".recs", idx.size() * 4);
+      // [n_rb + 1] row pointers | [n_tiles + 1] chunk pointers | row records | chunk records
+      r_ptr = recs;
+      c_ptr = recs + n_rb + 1;
+      r_rec = c_ptr + n_tiles + 1;
+      c_rec = r_rec + nrr;
       // pageable sources: the copies complete before cudaMemcpyAsync returns
       LGP_CUDA_CHECK(cudaMemcpyAsync(items, it.data(), it.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-      LGP_CUDA_CHECK(cudaMemcpyAsync(colbase, cb.data(), cb.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-      LGP_CUDA_CHECK(cudaMemcpyAsync(item0, f0.data(), f0.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-      LGP_CUDA_CHECK(cudaMemcpyAsync(nsegb, ns.data(), ns.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-      partial = (double*)ctx->scratch_get(tag + ".rowp", (size_t)n_items * 128 * 8);
-      colpart = (double*)ctx->scratch_get(tag + ".colp", (size_t)std::max<long long>(rec, 1) * 64 * 8);
-      if (item_lo != 0 || item_hi != n_items) {
-        // partial records of other ranks' items stay zero in this rank's sums
-        LGP_CUDA_CHECK(cudaMemsetAsync(partial, 0, (size_t)n_items * 128 * 8, ctx->stream));
-        LGP_CUDA_CHECK(cudaMemsetAsync(colpart, 0, (size_t)std::max<long long>(rec, 1) * 64 * 8, ctx->stream));
-      }
+      LGP_CUDA_CHECK(cudaMemcpyAsync(recs, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+      // partials of this rank's items only: one 128-row record per (item, row
+      // block), one 64-column record per (item, chunk)
+      partial = (double*)ctx->scratch_get(tag + ".rowp", (size_t)std::max(nrr, 1) * 128 * 8);
+      colpart = (double*)ctx->scratch_get(tag + ".colp", (size_t)std::max(ncr, 1) * 64 * 8);
       vpack = (double*)ctx->scratch_get(tag + ".v", (size_t)std::max(n_rows_pad, n_cols_pad) * 8);
     }
     return;
@@ -351,19 +436,21 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
       a.r32 = r32;
       a.c32 = c32;
       a.items = items;
-      a.colbase = colbase;
       a.rowpart = partial;
       a.colpart = colpart;
       a.done = done;
       a.item_base = item_lo;
+      a.R = ts_R;
+      a.n_rb = n_rb;
+      a.n_tiles = n_tiles;
       std::memcpy(a.kc, plan.tca.kc, sizeof a.kc);
       prof_begin();
       if (item_hi > item_lo)
         launch(ctx, mod->tcsym, (unsigned)(item_hi - item_lo), 1, 64 + 128 * plan.ts_nwg,
-               plan.smem_tcsym, &a);
+               plan.smem_tcsym_fixed + (size_t)2 * ts_R * 64 * 8, &a);
       prof_end();
-      vec::tcsym_epilogue(ctx, partial, colpart, item0, nsegb, colbase, n_rows, plan.root_scale,
-                          noise, noise_v, out_dev, done, blk_lo, blk_hi);
+      vec::tcsym_epilogue(ctx, partial, colpart, r_ptr, r_rec, c_ptr, c_rec, n_rows, plan.root_scale,
+                          noise, noise_v, out_dev, done);
       return;
     }
     vec::pack_rhs_tc(ctx, V_dev, cols->n, t, n_tiles, tb, n_pass, vtc, vscale, v_inexact, done);

@@ -103,7 +103,8 @@ struct Plan {
   int tc_fw = 0;            // FP32 features per point for FMA-pipe distance chunks
   int tc_pf = 0;            // of which Periodic (cos, sin) features, from offset P0
   bool tc_simt = false;     // some K1-TC chunks compute distances on the FMA pipe
-  size_t smem_tcsym = 0;    // dynamic shared memory of lgp_matvec_tcsym
+  size_t smem_tcsym = 0;    // dynamic shared memory of lgp_matvec_tcsym (at R = kTsRMax)
+  size_t smem_tcsym_fixed = 0;  // ... without the [2R][64] column accumulators
   int ts_nwg = 3;           // lgp_matvec_tcsym epilogue warpgroups
   bool tc_v5 = false;       // use lgp_matvec_tc4 (mma.sync distance tiles) for t > 1
   int t4_nwg = 4;
@@ -122,6 +123,9 @@ double r2_gain(const Tree& tree);
 // ~2^-22 (|c| + |c'|)^2 absolutely; point sets whose reach (in lengthscales)
 // exceeds this bound use direct differences instead (MatvecOp::prepare).
 constexpr double kNormTrickReach2 = 210.0;
+// K1-TC-sym super-tiles: at most this many row blocks per work item (its
+// [2R][64] FP64 column accumulators live in shared memory)
+constexpr int kTsRMax = 64;
 
 // A loaded JIT module.
 struct Module {
@@ -211,6 +215,14 @@ void comm_allreduce_sum_inplace(Comm* c, double* buf, size_t count, cudaStream_t
 void comm_allreduce_max_host(Comm* c, double* vals, int count, cudaStream_t stream);
 
 // ------------------------------------------------------ matvec engine
+// K1-TC-sym work item: row blocks [Ia, Ib) x 64-column chunks [ca, cb) of
+// the pair triangle c >= 2I, `pairs` (I, c) tiles of 128 x 64 entries
+struct TsRect {
+  int Ia, Ib, ca, cb;
+  int64_t pairs;
+};
+std::vector<TsRect> ts_items(int n_rb, int n_tiles, int R, int slots);
+
 // Device-resident matvec: out_rows[n_rows_local x t] for rows
 // [row0, row0+n_rows_local) of `rows` against all of `cols`.
 // V_dev: n_cols x t (device). out_dev: n_rows_local x t (device).
@@ -233,12 +245,11 @@ struct MatvecOp {
   // over ALL rows (K1-TC-sym), the per-rank products are all-reduced
   bool rank_split = false;
   int item_lo = 0, item_hi = 0;  // this rank's items [lo, hi) (rank_split)
-  int blk_lo = 0, blk_hi = 0;    // row blocks those items cover (inclusive)
   int n_items = 0;
-  int* items = nullptr;          // tcsym: [n_items][3]
-  long long* colbase = nullptr;  // tcsym: [n_rb]
-  int* item0 = nullptr;          // tcsym: [n_rb] first item / [n_rb] item count of each row block
-  int* nsegb = nullptr;
+  int ts_R = 1;                  // tcsym: max row blocks per item (record strides)
+  int* items = nullptr;          // tcsym: [n_items][4] = (Ia, Ib, ca, cb), launch order
+  int* recs = nullptr;           // tcsym: epilogue record lists (see prepare)
+  int *r_ptr = nullptr, *r_rec = nullptr, *c_ptr = nullptr, *c_rec = nullptr;
   int n_units = 0;
   int* units = nullptr;
   double* colpart = nullptr;
@@ -281,12 +292,13 @@ void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int 
 // UMMA K-major canonical layout
 void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int tbn, int n_pass,
                  void* out, float* scale, int* inexact, const int* done);
-// symmetric tensor-core K1 (t = 1): out_i = scale * (row partials of i's block
-// segments + column partials (I, chunk(i)) for I <= chunk(i) / 2) + noise * v_i
-void tcsym_epilogue(Context* c, const double* rowpart, const double* colpart, const int* item0,
-                    const int* nseg, const long long* colbase, int64_t n, double scale,
-                    double noise, const double* noise_v, double* out, const int* done,
-                    int blk_lo, int blk_hi);
+// symmetric tensor-core K1 (t = 1): out_i = scale * (column records of
+// chunk(i): c_rec[c_ptr[c] .. c_ptr[c+1]) + row records of block(i):
+// r_rec[r_ptr[I] .. r_ptr[I+1])) + noise * v_i, records in list order
+// (fixed order: deterministic)
+void tcsym_epilogue(Context* c, const double* rowpart, const double* colpart, const int* r_ptr,
+                    const int* r_rec, const int* c_ptr, const int* c_rec, int64_t n, double scale,
+                    double noise, const double* noise_v, double* out, const int* done);
 void epilogue(Context* c, const double* partial, int n_seg, int n_pass, int64_t rows_pad, int tb,
               int64_t n_rows, int t, double scale, double noise, const double* noise_v,
               double* out, const int* done);

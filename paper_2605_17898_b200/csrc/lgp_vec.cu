@@ -716,49 +716,38 @@ __global__ void k_pt_radius(const double* __restrict__ x, long long n, int d,
   if ((threadIdx.x & 31) == 0 && isfinite(m)) atomicMax(r2max, __double_as_longlong(m));
 }
 
-// One block per 64-column chunk c: out[64c + jj] = scale * (row partials of
-// that row over its segments + column partials of chunk c over the row blocks
-// I2 <= c / 2) + noise * v. The column sum (up to N / 128 terms) is split over
-// kTsGroups thread groups (I2 = g, g + G, ...) and combined in g order: fixed
-// order, deterministic. (One thread per output walking all I2 serially was
-// latency-bound: 125 us at cfg4 for 259 MB of partials.)
+// One block per 64-column chunk c: out[64c + jj] = scale * (the column
+// records of chunk c + the row records of row block I = c / 2) + noise * v.
+// Each side's sum is split over kTsGroups thread groups (group g takes list
+// entries g, g + G, ...) and combined in g order, column side first: fixed
+// order, deterministic.
 constexpr int kTsGroups = 8;
 __global__ void __launch_bounds__(64 * kTsGroups)
     k_tcsym_epilogue(const double* __restrict__ rowpart, const double* __restrict__ colpart,
-                     const int* __restrict__ item0, const int* __restrict__ nseg,
-                     const long long* __restrict__ colbase, long long n, double scale,
-                     double noise, const double* __restrict__ noise_v, double* __restrict__ out,
-                     const int* done, int blk_lo, int blk_hi) {
-  __shared__ double part[kTsGroups][64];
+                     const int* __restrict__ r_ptr, const int* __restrict__ r_rec,
+                     const int* __restrict__ c_ptr, const int* __restrict__ c_rec, long long n,
+                     double scale, double noise, const double* __restrict__ noise_v,
+                     double* __restrict__ out, const int* done) {
+  __shared__ double part[2][kTsGroups][64];
   if (is_done(done)) return;
-  const long long c = blockIdx.x;
+  const int c = blockIdx.x;
   const int jj = threadIdx.x & 63, g = threadIdx.x >> 6;
-  // only row blocks [blk_lo, blk_hi] carry records (a rank's share of the
-  // pair items in the multi-rank CG; all blocks on one rank)
-  const long long last = (c >> 1) < blk_hi ? (c >> 1) : blk_hi;
   double s = 0.0;
-  long long I2 = blk_lo + g;
-  for (; I2 + 3 * kTsGroups <= last; I2 += 4 * kTsGroups) {
-    double v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const long long J = I2 + u * kTsGroups;
-      v[u] = colpart[(size_t)(colbase[J] + c - 2 * J) * 64 + jj];
-    }
-    s = (((s + v[0]) + v[1]) + v[2]) + v[3];
-  }
-  for (; I2 <= last; I2 += kTsGroups) s += colpart[(size_t)(colbase[I2] + c - 2 * I2) * 64 + jj];
-  part[g][jj] = s;
+  for (int e = c_ptr[c] + g; e < c_ptr[c + 1]; e += kTsGroups) s += colpart[(size_t)c_rec[e] * 64 + jj];
+  part[0][g][jj] = s;
+  const int I = c >> 1, r = (c & 1) * 64 + jj;
+  double t = 0.0;
+  for (int e = r_ptr[I] + g; e < r_ptr[I + 1]; e += kTsGroups) t += rowpart[(size_t)r_rec[e] * 128 + r];
+  part[1][g][jj] = t;
   __syncthreads();
-  const long long i = c * 64 + jj;
+  const long long i = (long long)c * 64 + jj;
   if (g == 0 && i < n) {
-    const int I = (int)(c >> 1), r = (int)((c & 1) * 64 + jj);
-    const int f = item0[I], m = (I >= blk_lo && I <= blk_hi) ? nseg[I] : 0;
-    double t = 0.0;
-    for (int k = 0; k < m; ++k) t += rowpart[(size_t)(f + k) * 128 + r];
+    double o = 0.0;
 #pragma unroll
-    for (int u = 0; u < kTsGroups; ++u) t += part[u][jj];
-    double o = __dmul_rn(scale, t);
+    for (int u = 0; u < kTsGroups; ++u) o += part[0][u][jj];
+#pragma unroll
+    for (int u = 0; u < kTsGroups; ++u) o += part[1][u][jj];
+    o = __dmul_rn(scale, o);
     if (noise_v != nullptr && noise != 0.0) o = __dadd_rn(o, __dmul_rn(noise, noise_v[i]));
     out[i] = o;
   }
@@ -816,13 +805,12 @@ void pack_rhs_tc(Context* c, const double* V, int64_t n, int t, int n_tiles, int
   LGP_LAUNCH_CHECK(c);
 }
 
-void tcsym_epilogue(Context* c, const double* rowpart, const double* colpart, const int* item0,
-                    const int* nseg, const long long* colbase, int64_t n, double scale,
-                    double noise, const double* noise_v, double* out, const int* done,
-                    int blk_lo, int blk_hi) {
+void tcsym_epilogue(Context* c, const double* rowpart, const double* colpart, const int* r_ptr,
+                    const int* r_rec, const int* c_ptr, const int* c_rec, int64_t n, double scale,
+                    double noise, const double* noise_v, double* out, const int* done) {
   if (n <= 0) return;
   k_tcsym_epilogue<<<(unsigned)((n + 63) / 64), 64 * kTsGroups, 0, c->stream>>>(
-      rowpart, colpart, item0, nseg, colbase, n, scale, noise, noise_v, out, done, blk_lo, blk_hi);
+      rowpart, colpart, r_ptr, r_rec, c_ptr, c_rec, n, scale, noise, noise_v, out, done);
   LGP_LAUNCH_CHECK(c);
 }
 
