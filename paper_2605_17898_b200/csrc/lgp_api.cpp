@@ -209,6 +209,9 @@ int lgp_ctx_destroy(lgp_ctx* ctx) {
   for (auto& kv : ctx->modules)
     if (kv.second->mod) drv::ModuleUnload(kv.second->mod);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+  if (ctx->done_pin) cudaFreeHost(ctx->done_pin);
+  for (cudaEvent_t e : ctx->done_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& kv : ctx->pool)
     for (void* q : kv.second) cudaFree(q);
   for (auto& ev : ctx->ev_pending) ctx->ev_pool.push_back(ev);

@@ -144,6 +144,104 @@ void launch(Context* ctx, CUfunction f, unsigned gx, unsigned gy, unsigned bx, s
 }
 }  // namespace
 
+// K1-TC-sym work schedule for an n_rb x n_tiles square operator (host
+// side; cached per context: the list-scheduling model and the record lists
+// cost milliseconds at N ~ 1e5 and the CG / Lanczos drivers prepare per call)
+const TsSchedule& ts_schedule(Context* ctx, int n_rb, int n_tiles, int rmax, bool rank_split) {
+  const char* fe = std::getenv("LGP_TS_R");
+  const std::string key = std::to_string(n_rb) + "/" + std::to_string(n_tiles) + "/" + std::to_string(rmax) +
+                      "/" + std::to_string(rank_split && ctx->world > 1 ? ctx->world : 1) + "/" +
+                      std::to_string(ctx->rank) + "/" + (fe ? fe : "");
+  auto hit = ctx->ts_cache.find(key);
+  if (hit != ctx->ts_cache.end()) return *hit->second;
+  auto out = std::make_shared<TsSchedule>();
+  TsSchedule& S = *out;
+  // work items: rectangles of the (row block, chunk) triangle c >= 2I -
+  // R x 2R super-tiles (full ones first, the diagonal ones after), the
+  // ones dispatched in the last two waves split into quarters; R picked
+  // by a list-scheduling model of the items on the SMs (one CTA per SM)
+  // so the items fill whole waves while the scratch (R x 128 + 2R x 64
+  // doubles per item) stays O(N)
+  int R = 1;
+  std::vector<TsRect> rects;
+  {
+    const int cands[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64};
+    double best = 1e300;
+    int forced = 0;
+    if (const char* e = std::getenv("LGP_TS_R")) forced = std::max(1, std::min(rmax, atoi(e)));
+    for (int Rc : cands) {
+      if (Rc > rmax) break;
+      if (forced && Rc != forced) continue;
+      const int64_t nG = ceil_div<int64_t>(n_rb, Rc);
+      if (nG * (nG + 1) / 2 > 2000000) continue;
+      std::vector<TsRect> rc = ts_items(n_rb, n_tiles, Rc, ctx->sm_count);
+      const double span = ts_makespan(rc, ctx->sm_count);
+      if (span < best * 0.995) {  // near-ties: the larger R (less scratch)
+        best = span;
+        R = Rc;
+        rects.swap(rc);
+      } else if (span <= best * 1.005) {
+        R = Rc;
+        rects.swap(rc);
+      }
+    }
+    if (forced) R = forced;
+  }
+  const int n_items = (int)rects.size();
+  int item_lo = 0, item_hi = n_items;
+  if (rank_split && ctx->world > 1) {
+    // contiguous item ranges with (nearly) equal pair counts per rank
+    int64_t total = 0;
+    for (const TsRect& r : rects) total += r.pairs;
+    int64_t acc = 0;
+    int r = 0;
+    std::vector<int> cut(ctx->world + 1, n_items);
+    cut[0] = 0;
+    for (int q = 0; q < n_items; ++q) {
+      while (r < ctx->world - 1 && acc >= (int64_t)(r + 1) * total / ctx->world) cut[++r] = q;
+      acc += rects[q].pairs;
+    }
+    item_lo = cut[ctx->rank];
+    item_hi = cut[ctx->rank + 1];
+  }
+  // item table (Ia, Ib, ca, cb, first row record, first chunk record) +
+  // the records each row block / chunk sums (this rank's items, in item
+  // order: the epilogue's fixed summation order)
+  std::vector<int> it((size_t)n_items * 6);
+  std::vector<std::vector<int>> rl(n_rb), cl(n_tiles);
+  int nrr = 0, ncr = 0;
+  for (int q = 0; q < n_items; ++q) {
+    const TsRect& r = rects[q];
+    it[6 * q] = r.Ia;
+    it[6 * q + 1] = r.Ib;
+    it[6 * q + 2] = r.ca;
+    it[6 * q + 3] = r.cb;
+    it[6 * q + 4] = nrr;
+    it[6 * q + 5] = ncr;
+    if (q < item_lo || q >= item_hi) continue;
+    for (int I = r.Ia; I < r.Ib; ++I) rl[I].push_back(nrr++);
+    for (int c = r.ca; c < r.cb; ++c) cl[c].push_back(ncr++);
+  }
+  std::vector<int> idx;
+  idx.reserve((size_t)n_rb + n_tiles + 2 + nrr + ncr);
+  idx.push_back(0);
+  for (int I = 0; I < n_rb; ++I) idx.push_back(idx.back() + (int)rl[I].size());
+  idx.push_back(0);
+  for (int c = 0; c < n_tiles; ++c) idx.push_back(idx.back() + (int)cl[c].size());
+  for (int I = 0; I < n_rb; ++I) idx.insert(idx.end(), rl[I].begin(), rl[I].end());
+  for (int c = 0; c < n_tiles; ++c) idx.insert(idx.end(), cl[c].begin(), cl[c].end());
+  S.R = R;
+  S.n_items = n_items;
+  S.item_lo = item_lo;
+  S.item_hi = item_hi;
+  S.nrr = nrr;
+  S.ncr = ncr;
+  S.it.swap(it);
+  S.idx.swap(idx);
+  ctx->ts_cache[key] = out;
+  return S;
+}
+
 void MatvecOp::prepare() {
   int tb = pick_tb(t);
   {
@@ -168,7 +266,7 @@ void MatvecOp::prepare() {
   if (t == 1 && rows == cols && (!ctx->sharded() || rank_split) && row0 == 0 && n_rows == rows->n &&
       !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && !std::getenv("LGP_NO_TCSYM")) {
     Plan p = make_tc_plan(k->tree, rows->d, 16, flags);
-    if (p.tc && !p.tc_pair) {
+    if (p.tc && !p.tc_pair && p.ts_rmax >= 1) {
       plan = p;
       tcsym = true;
     }
@@ -257,82 +355,14 @@ void MatvecOp::prepare() {
                                    128, 1, 1, 0, (CUstream)ctx->stream, p2, nullptr));
     ++ctx->launches;
     if (tcsym) {
-      // work items: rectangles of the (row block, chunk) triangle c >= 2I -
-      // R x 2R super-tiles (full ones first, the diagonal ones after), the
-      // ones dispatched in the last two waves split into quarters; R picked
-      // by a list-scheduling model of the items on the SMs (one CTA per SM)
-      // so the items fill whole waves while the scratch (R x 128 + 2R x 64
-      // doubles per item) stays O(N)
-      int R = 1;
-      std::vector<TsRect> rects;
-      {
-        const int cands[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64};
-        double best = 1e300;
-        int forced = 0;
-        if (const char* e = std::getenv("LGP_TS_R")) forced = std::max(1, std::min(kTsRMax, atoi(e)));
-        for (int Rc : cands) {
-          if (Rc > kTsRMax) break;
-          if (forced && Rc != forced) continue;
-          const int64_t nG = ceil_div<int64_t>(n_rb, Rc);
-          if (nG * (nG + 1) / 2 > 2000000) continue;
-          std::vector<TsRect> rc = ts_items(n_rb, n_tiles, Rc, ctx->sm_count);
-          const double span = ts_makespan(rc, ctx->sm_count);
-          if (span < best * 0.995) {  // near-ties: the larger R (less scratch)
-            best = span;
-            R = Rc;
-            rects.swap(rc);
-          } else if (span <= best * 1.005) {
-            R = Rc;
-            rects.swap(rc);
-          }
-        }
-        if (forced) R = forced;
-      }
-      n_items = (int)rects.size();
-      ts_R = R;
-      item_lo = 0;
-      item_hi = n_items;
-      if (rank_split && ctx->world > 1) {
-        // contiguous item ranges with (nearly) equal pair counts per rank
-        int64_t total = 0;
-        for (const TsRect& r : rects) total += r.pairs;
-        int64_t acc = 0;
-        int r = 0;
-        std::vector<int> cut(ctx->world + 1, n_items);
-        cut[0] = 0;
-        for (int q = 0; q < n_items; ++q) {
-          while (r < ctx->world - 1 && acc >= (int64_t)(r + 1) * total / ctx->world) cut[++r] = q;
-          acc += rects[q].pairs;
-        }
-        item_lo = cut[ctx->rank];
-        item_hi = cut[ctx->rank + 1];
-      }
-      // item table (Ia, Ib, ca, cb, first row record, first chunk record) +
-      // the records each row block / chunk sums (this rank's items, in item
-      // order: the epilogue's fixed summation order)
-      std::vector<int> it((size_t)n_items * 6);
-      std::vector<std::vector<int>> rl(n_rb), cl(n_tiles);
-      int nrr = 0, ncr = 0;
-      for (int q = 0; q < n_items; ++q) {
-        const TsRect& r = rects[q];
-        it[6 * q] = r.Ia;
-        it[6 * q + 1] = r.Ib;
-        it[6 * q + 2] = r.ca;
-        it[6 * q + 3] = r.cb;
-        it[6 * q + 4] = nrr;
-        it[6 * q + 5] = ncr;
-        if (q < item_lo || q >= item_hi) continue;
-        for (int I = r.Ia; I < r.Ib; ++I) rl[I].push_back(nrr++);
-        for (int c = r.ca; c < r.cb; ++c) cl[c].push_back(ncr++);
-      }
-      std::vector<int> idx;
-      idx.reserve((size_t)n_rb + n_tiles + 2 + nrr + ncr);
-      idx.push_back(0);
-      for (int I = 0; I < n_rb; ++I) idx.push_back(idx.back() + (int)rl[I].size());
-      idx.push_back(0);
-      for (int c = 0; c < n_tiles; ++c) idx.push_back(idx.back() + (int)cl[c].size());
-      for (int I = 0; I < n_rb; ++I) idx.insert(idx.end(), rl[I].begin(), rl[I].end());
-      for (int c = 0; c < n_tiles; ++c) idx.insert(idx.end(), cl[c].begin(), cl[c].end());
+      const TsSchedule& sc = ts_schedule(ctx, n_rb, n_tiles, plan.ts_rmax, rank_split);
+      n_items = sc.n_items;
+      ts_R = sc.R;
+      item_lo = sc.item_lo;
+      item_hi = sc.item_hi;
+      const int nrr = sc.nrr, ncr = sc.ncr;
+      const std::vector<int>& it = sc.it;
+      const std::vector<int>& idx = sc.idx;
       items = (int*)ctx->scratch_get(tag + ".items", it.size() * 4);
       recs = (int*)ctx->scratch_get(tag + ".recs", idx.size() * 4);
       // [n_rb + 1] row pointers | [n_tiles + 1] chunk pointers | row records | chunk records
@@ -404,50 +434,61 @@ void MatvecOp::prepare() {
   launch(ctx, mod->prep, (unsigned)ceil_div<int64_t>(n_cols_pad, 128), 1, 128, 0, &pc);
 }
 
+// per-launch CUDA events around the fused K1 kernel (lgp_ctx_set_profile)
+std::pair<cudaEvent_t, cudaEvent_t> k1_event_begin(Context* ctx) {
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (!ctx->profile) return ev;
+  if (ctx->ev_pool.empty()) {
+    LGP_CUDA_CHECK(cudaEventCreate(&ev.first));
+    LGP_CUDA_CHECK(cudaEventCreate(&ev.second));
+  } else {
+    ev = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+  }
+  LGP_CUDA_CHECK(cudaEventRecord(ev.first, ctx->stream));
+  return ev;
+}
+
+void k1_event_end(Context* ctx, std::pair<cudaEvent_t, cudaEvent_t> ev) {
+  if (!ctx->profile || !ev.first) return;
+  LGP_CUDA_CHECK(cudaEventRecord(ev.second, ctx->stream));
+  ctx->ev_pending.push_back(ev);
+}
+
+void MatvecOp::tcsym_kernel(const int* done) {
+  LgpTcSymArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.a1 = fr;
+  a.b1 = fc;
+  a.v = vpack;
+  a.r32 = r32;
+  a.c32 = c32;
+  a.items = items;
+  a.rowpart = partial;
+  a.colpart = colpart;
+  a.done = done;
+  a.item_base = item_lo;
+  a.R = ts_R;
+  a.n_rb = n_rb;
+  a.n_tiles = n_tiles;
+  std::memcpy(a.kc, plan.tca.kc, sizeof a.kc);
+  if (item_hi > item_lo)
+    launch(ctx, mod->tcsym, (unsigned)(item_hi - item_lo), 1, 64 + 128 * plan.ts_nwg,
+           plan.smem_tcsym_fixed + (size_t)2 * ts_R * 64 * 8, &a);
+}
+
 void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const double* noise_v,
                    const int* done) {
   const int tb = plan.tune.tb;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-  auto prof_begin = [&]() {
-    if (!ctx->profile) return;
-    if (ctx->ev_pool.empty()) {
-      LGP_CUDA_CHECK(cudaEventCreate(&ev.first));
-      LGP_CUDA_CHECK(cudaEventCreate(&ev.second));
-    } else {
-      ev = ctx->ev_pool.back();
-      ctx->ev_pool.pop_back();
-    }
-    LGP_CUDA_CHECK(cudaEventRecord(ev.first, ctx->stream));
-  };
-  auto prof_end = [&]() {
-    if (!ctx->profile) return;
-    LGP_CUDA_CHECK(cudaEventRecord(ev.second, ctx->stream));
-    ctx->ev_pending.push_back(ev);
-  };
+  auto prof_begin = [&]() { ev = k1_event_begin(ctx); };
+  auto prof_end = [&]() { k1_event_end(ctx, ev); };
   if (plan.tc) {
     if (tcsym) {
       const int npad = std::max(n_rows_pad, n_cols_pad);
       vec::pack_rhs(ctx, V_dev, cols->n, 1, npad, 1, 1, vpack, done);
-      LgpTcSymArgs a;
-      std::memset(&a, 0, sizeof a);
-      a.a1 = fr;
-      a.b1 = fc;
-      a.v = vpack;
-      a.r32 = r32;
-      a.c32 = c32;
-      a.items = items;
-      a.rowpart = partial;
-      a.colpart = colpart;
-      a.done = done;
-      a.item_base = item_lo;
-      a.R = ts_R;
-      a.n_rb = n_rb;
-      a.n_tiles = n_tiles;
-      std::memcpy(a.kc, plan.tca.kc, sizeof a.kc);
       prof_begin();
-      if (item_hi > item_lo)
-        launch(ctx, mod->tcsym, (unsigned)(item_hi - item_lo), 1, 64 + 128 * plan.ts_nwg,
-               plan.smem_tcsym_fixed + (size_t)2 * ts_R * 64 * 8, &a);
+      tcsym_kernel(done);
       prof_end();
       vec::tcsym_epilogue(ctx, partial, colpart, r_ptr, r_rec, c_ptr, c_rec, n_rows, plan.root_scale,
                           noise, noise_v, out_dev, done);
@@ -550,6 +591,42 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
 }
 
 // ------------------------------------------------------------------ CG
+DonePoller::DonePoller(Context* c, const int* d, int a) : ctx(c), done_dev(d), ahead(std::max(1, std::min(a, 15))) {
+  if (!ctx->done_pin) LGP_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->done_pin), 16 * sizeof(int), 0));
+  for (cudaEvent_t& e : ctx->done_ev)
+    if (!e) LGP_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+bool DonePoller::check() {
+  const int slot = tail % 16;
+  LGP_CUDA_CHECK(cudaMemcpyAsync(ctx->done_pin + slot, done_dev, sizeof(int), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  LGP_CUDA_CHECK(cudaEventRecord(ctx->done_ev[slot], ctx->stream));
+  ++tail;
+  while (head < tail) {
+    const int h = head % 16;
+    if (tail - head > ahead) {
+      LGP_CUDA_CHECK(cudaEventSynchronize(ctx->done_ev[h]));
+    } else {
+      const cudaError_t q = cudaEventQuery(ctx->done_ev[h]);
+      if (q == cudaErrorNotReady) break;
+      LGP_CUDA_CHECK(q);
+    }
+    ++head;
+    if (ctx->done_pin[h]) return true;
+  }
+  return false;
+}
+
+bool DonePoller::drain() {
+  bool any = false;
+  for (; head < tail; ++head) {
+    LGP_CUDA_CHECK(cudaEventSynchronize(ctx->done_ev[head % 16]));
+    any = any || ctx->done_pin[head % 16] != 0;
+  }
+  return any;
+}
+
 struct CgBuffers {
   double *x, *r, *p, *ap, *part, *bb;
   vec::CgState s;
@@ -642,16 +719,48 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   // host-side stop checks: every iteration for large operators, else in
   // batches (kernels after convergence early-exit on the device flag)
   const double entries = (double)n * (double)n * t;
-  // the host reads the device done flag every few iterations: a per-iteration
-  // round trip leaves the GPU idle between iterations (~30 us at cfg4), while
-  // iterations enqueued past convergence exit at their first instruction
-  int check_every = entries > 2e8 ? 4 : 8;
+  // the host samples the device done flag every few iterations through
+  // asynchronous copies (DonePoller): it never waits for the GPU to drain
+  // (a synchronous check every 4 iterations left it idle ~30 us each time),
+  // and iterations enqueued past convergence exit at their first instruction
+  int check_every = entries > 2e8 ? 2 : 8;
   if (const char* e = std::getenv("LGP_CG_CHECK")) check_every = std::max(1, atoi(e));
+  DonePoller poll(ctx, b.s.done, entries > 2e8 ? 2 : 4);
   int done_h = 0;
   LGP_CUDA_CHECK(cudaMemcpyAsync(&done_h, b.s.done, sizeof(int), cudaMemcpyDeviceToHost,
                                  ctx->stream));
   LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  // single RHS on the symmetric tensor-core kernel: the fused iteration (4
+  // launches: pack+p-update, K1, records+p.Ap+step, x/r update+r.r+beta)
+  const bool fused = op.tcsym && t == 1 && !std::getenv("LGP_CG_UNFUSED");
+  double* part1 = nullptr;
+  unsigned* cnt1 = nullptr;
+  if (fused) {
+    const size_t np = (size_t)std::max<int64_t>(op.n_tiles, vec::cg1_blocks(n));
+    part1 = (double*)ctx->scratch_get("cg.part1", np * 8 + 16);
+    cnt1 = reinterpret_cast<unsigned*>(part1 + np);
+    LGP_CUDA_CHECK(cudaMemsetAsync(cnt1, 0, 16, ctx->stream));
+  }
   for (int it = 1; it <= max_iter && !done_h; ++it) {
+    if (fused) {
+      vec::cg1_pack(ctx, b.p, b.r, op.vpack, n, std::max(op.n_rows_pad, op.n_cols_pad), b.s);
+      {
+        auto ev = k1_event_begin(ctx);
+        op.tcsym_kernel(b.s.done);
+        k1_event_end(ctx, ev);
+      }
+      if (split) {
+        vec::tcsym_epilogue(ctx, op.partial, op.colpart, op.r_ptr, op.r_rec, op.c_ptr, op.c_rec, n,
+                            op.plan.root_scale, ctx->rank == 0 ? noise : 0.0,
+                            ctx->rank == 0 ? b.p : nullptr, b.ap, b.s.done);
+        comm_allreduce_sum_inplace(ctx->comm, b.ap, (size_t)n, ctx->stream);
+        vec::cg1_pap(ctx, b.p, b.ap, n, part1, cnt1, b.s);
+      } else {
+        vec::tcsym_epilogue_cg(ctx, op.partial, op.colpart, op.r_ptr, op.r_rec, op.c_ptr, op.c_rec, n,
+                               op.plan.root_scale, noise, b.p, b.ap, part1, cnt1, b.s);
+      }
+      vec::cg1_update(ctx, b.x, b.r, b.p, b.ap, n, part1, cnt1, it, max_iter, b.s);
+    } else {
     if (split) {
       // this rank's pair share over all rows (noise term on rank 0 only), then
       // the sum over ranks: one all-reduce of n doubles per iteration
@@ -666,12 +775,10 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
     vec::cg_update_xr(ctx, b.x, b.r, b.p, b.ap, n, t, b.s, b.part);
     vec::cg_fin_rs(ctx, b.part, nblk, t, it, max_iter, b.s);
     vec::cg_update_p(ctx, b.p, b.r, n, t, b.s);
-    if (it % check_every == 0 || it == max_iter) {
-      LGP_CUDA_CHECK(cudaMemcpyAsync(&done_h, b.s.done, sizeof(int), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
-      LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     }
+    if (it % check_every == 0 || it == max_iter) done_h = poll.check();
   }
+  poll.drain();
   int status[2] = {0, -1};
   LGP_CUDA_CHECK(cudaMemcpyAsync(status, b.s.status, 2 * sizeof(int), cudaMemcpyDeviceToHost,
                                  ctx->stream));
@@ -732,11 +839,13 @@ void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, doub
   vec::lz_init(ctx, Z_dev, basis, n, t, zz, s);
   const int64_t stride = (int64_t)n_alloc * t;
   const double entries = (double)n * (double)n * t;
-  // the host reads the device done flag every few iterations: a per-iteration
-  // round trip leaves the GPU idle between iterations (~30 us at cfg4), while
-  // iterations enqueued past convergence exit at their first instruction
-  int check_every = entries > 2e8 ? 4 : 8;
+  // the host samples the device done flag every few iterations through
+  // asynchronous copies (DonePoller): it never waits for the GPU to drain
+  // (a synchronous check every 4 iterations left it idle ~30 us each time),
+  // and iterations enqueued past convergence exit at their first instruction
+  int check_every = entries > 2e8 ? 2 : 8;
   if (const char* e = std::getenv("LGP_CG_CHECK")) check_every = std::max(1, atoi(e));
+  DonePoller poll(ctx, s.done, entries > 2e8 ? 2 : 4);
   int done_h = 0;
   for (int j = 0; j < steps && !done_h; ++j) {
     double* q = basis + (size_t)j * stride;
@@ -752,12 +861,9 @@ void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, doub
     vec::lz_update2(ctx, w, basis, stride, j + 1, n, t, s, part);
     vec::lz_fin_beta(ctx, part, nblk, t, j, steps, s);
     vec::lz_normalize(ctx, w, basis + (size_t)(j + 1) * stride, n, t, s);
-    if ((j + 1) % check_every == 0) {
-      LGP_CUDA_CHECK(cudaMemcpyAsync(&done_h, s.done, sizeof(int), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
-      LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    }
+    if ((j + 1) % check_every == 0) done_h = poll.check();
   }
+  poll.drain();
   std::vector<double> al((size_t)t * steps), be((size_t)t * steps);
   LGP_CUDA_CHECK(cudaMemcpyAsync(al.data(), s.alpha, al.size() * 8, cudaMemcpyDeviceToHost,
                                  ctx->stream));

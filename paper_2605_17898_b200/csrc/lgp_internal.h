@@ -105,6 +105,7 @@ struct Plan {
   bool tc_simt = false;     // some K1-TC chunks compute distances on the FMA pipe
   size_t smem_tcsym = 0;    // dynamic shared memory of lgp_matvec_tcsym (at R = kTsRMax)
   size_t smem_tcsym_fixed = 0;  // ... without the [2R][64] column accumulators
+  int ts_rmax = 0;              // largest super-tile R that fits the shared memory
   int ts_nwg = 3;           // lgp_matvec_tcsym epilogue warpgroups
   bool tc_v5 = false;       // use lgp_matvec_tc4 (mma.sync distance tiles) for t > 1
   int t4_nwg = 4;
@@ -151,6 +152,20 @@ struct DeviceBuffer {
 
 struct Comm;  // NCCL communicator (dlopen'ed), null for world == 1
 
+// K1-TC-sym work item: row blocks [Ia, Ib) x 64-column chunks [ca, cb) of
+// the pair triangle c >= 2I, `pairs` (I, c) tiles of 128 x 64 entries
+struct TsRect {
+  int Ia, Ib, ca, cb;
+  int64_t pairs;
+};
+std::vector<TsRect> ts_items(int n_rb, int n_tiles, int R, int slots);
+// the items of one operator shape: R, this rank's item range, the item table
+// [n_items][6] and the record lists of the epilogue (see MatvecOp::prepare)
+struct TsSchedule {
+  int R = 1, n_items = 0, item_lo = 0, item_hi = 0, nrr = 0, ncr = 0;
+  std::vector<int> it, idx;
+};
+
 struct Context {
   int device = 0;
   int rank = 0;
@@ -166,8 +181,11 @@ struct Context {
   std::recursive_mutex mu;
   std::map<std::string, std::unique_ptr<Module>> modules;
   std::map<std::string, DeviceBuffer> scratch;
+  std::map<std::string, std::shared_ptr<TsSchedule>> ts_cache;  // K1-TC-sym schedules
   uint64_t launches = 0;
   void* flush_buf = nullptr;
+  int* done_pin = nullptr;               // pinned ring of device done-flag copies (solver loops)
+  cudaEvent_t done_ev[16] = {};          // ... and their completion events
   size_t flush_bytes = 0;
   // K1 timing (lgp_ctx_set_profile): event pairs around every fused-matvec
   // launch, on the launching stream
@@ -185,6 +203,8 @@ struct Context {
   void* scratch_get(const std::string& name, size_t bytes);  // grow-only
   void activate();  // cudaSetDevice for the calling thread
 };
+const TsSchedule& ts_schedule(Context* ctx, int n_rb, int n_tiles, int rmax, bool rank_split);
+
 
 struct KernelHandle {
   Context* ctx;
@@ -215,13 +235,7 @@ void comm_allreduce_sum_inplace(Comm* c, double* buf, size_t count, cudaStream_t
 void comm_allreduce_max_host(Comm* c, double* vals, int count, cudaStream_t stream);
 
 // ------------------------------------------------------ matvec engine
-// K1-TC-sym work item: row blocks [Ia, Ib) x 64-column chunks [ca, cb) of
-// the pair triangle c >= 2I, `pairs` (I, c) tiles of 128 x 64 entries
-struct TsRect {
-  int Ia, Ib, ca, cb;
-  int64_t pairs;
-};
-std::vector<TsRect> ts_items(int n_rb, int n_tiles, int R, int slots);
+
 
 // Device-resident matvec: out_rows[n_rows_local x t] for rows
 // [row0, row0+n_rows_local) of `rows` against all of `cols`.
@@ -270,9 +284,28 @@ struct MatvecOp {
   void prepare();  // features, scratch, schedule
   void run(const double* V_dev, double* out_dev, double noise, const double* noise_v,
            const int* done);
+  // K1-TC-sym alone, on the already packed vpack (fused CG iteration)
+  void tcsym_kernel(const int* done);
 };
 
 // ------------------------------------------------------ solver drivers
+// Host view of a solver loop's device `done` flag without stalling the GPU:
+// check() queues an asynchronous copy of the flag into pinned memory (+ an
+// event) and returns true once an already completed copy shows the flag set;
+// at most `ahead` copies stay in flight (the host then waits for the oldest),
+// so the host runs a bounded number of iterations ahead and iterations
+// enqueued past convergence exit at their first instruction.
+struct DonePoller {
+  Context* ctx;
+  const int* done_dev;
+  int ahead;
+  int head = 0, tail = 0;  // queued copies [head, tail) in the ring
+  DonePoller(Context* c, const int* d, int a);
+  bool check();
+  bool drain();  // wait for every queued copy; true if any shows done
+};
+std::pair<cudaEvent_t, cudaEvent_t> k1_event_begin(Context* ctx);
+void k1_event_end(Context* ctx, std::pair<cudaEvent_t, cudaEvent_t> ev);
 void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double noise,
                const double* B_dev, int t, double rel_tol, int max_iter, double** x_dev,
                int32_t* iters_out, double* res_out);
@@ -333,6 +366,20 @@ struct CgState {
 void cg_init(Context* c, const double* b, double* x, double* r, double* p, int64_t n, int t,
              double rel_tol, const double* bb_final, CgState s);
 void cg_fin_pap(Context* c, const double* part, int nblk, int t, CgState s);
+// fused single-RHS CG (4 launches per iteration, see lgp_vec.cu): part holds
+// the per-block shares (>= max(n_tiles, cg1_blocks(n)) doubles), counter one
+// zero-initialised unsigned (each fused kernel's last block resets it)
+void cg1_pack(Context* c, double* p, const double* r, double* vpack, int64_t n, int64_t n_pad,
+              CgState s);
+void tcsym_epilogue_cg(Context* c, const double* rowpart, const double* colpart, const int* r_ptr,
+                       const int* r_rec, const int* c_ptr, const int* c_rec, int64_t n,
+                       double scale, double noise, const double* p, double* out, double* part,
+                       unsigned* counter, CgState s);
+int cg1_blocks(int64_t n);
+void cg1_pap(Context* c, const double* p, const double* ap, int64_t n, double* part,
+             unsigned* counter, CgState s);
+void cg1_update(Context* c, double* x, double* r, const double* p, const double* ap, int64_t n,
+                double* part, unsigned* counter, int it, int max_iter, CgState s);
 void cg_update_xr(Context* c, double* x, double* r, const double* p, const double* ap, int64_t n,
                   int t, CgState s, double* part);
 void cg_fin_rs(Context* c, const double* part, int nblk, int t, int it, int max_iter, CgState s);

@@ -182,8 +182,9 @@ Module* get_module(Context* ctx, const Plan& plan) {
         LGP_CU_CHECK(drv::FuncSetAttribute(m->tc4, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                                            (int)plan.smem_tc4));
       }
-      LGP_CU_CHECK(drv::FuncSetAttribute(m->tcsym, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                                         (int)plan.smem_tcsym));
+      if (plan.smem_tcsym > 0)
+        LGP_CU_CHECK(drv::FuncSetAttribute(m->tcsym, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                           (int)plan.smem_tcsym));
     }
   } else {
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->prep, m->mod, "lgp_prep"));

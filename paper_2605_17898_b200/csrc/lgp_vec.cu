@@ -16,6 +16,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "lgp_internal.h"
@@ -28,10 +29,33 @@ namespace {
 // every SM streaming (n = 100k -> 391 blocks of 256 rows)
 constexpr int kMaxBlocks = 2048;
 constexpr int kRowsPerBlock = 256;
+// thread groups of the K1-TC-sym record epilogue (64 threads each)
+constexpr int kTsGroups = 8;
 
 inline int reduce_bd(int t) { return t * (256 / t); }
 
 __device__ __forceinline__ bool is_done(const int* done) { return done != nullptr && *done; }
+
+// sum of the records rec[e0 + g], rec[e0 + g + G], ... (< e1) at stride
+// `width` doubles, column jj: 4 loads in flight per round, fixed order
+template <int width>
+__device__ __forceinline__ double sum_records(const double* __restrict__ data, const int* __restrict__ rec,
+                                             int e0, int e1, int g, int jj) {
+  double s = 0.0;
+  int e = e0 + g;
+  for (; e + 3 * kTsGroups < e1; e += 4 * kTsGroups) {
+    int r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = __ldg(rec + e + u * kTsGroups);
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = data[(size_t)r[u] * width + jj];
+    s = (((s + v[0]) + v[1]) + v[2]) + v[3];
+  }
+  for (; e < e1; e += kTsGroups) s += data[(size_t)__ldg(rec + e) * width + jj];
+  return s;
+}
+
 
 // block partial of sum_i a[i][c]*b[i][c] over this block's row range -> part[blk][c]
 __device__ __forceinline__ void block_colsum(double v, int t, double* part_row, double* sm) {
@@ -370,6 +394,173 @@ __global__ void k_cg_update_p(double* __restrict__ p, const double* __restrict__
        e += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(e % t);
     if (s.active[c]) p[e] = __dadd_rn(__dmul_rn(p[e], s.beta[c]), r[e]);
+  }
+}
+
+// ------------------------------------------------- fused single-RHS CG
+// The alpha solve (t = 1) runs 4 launches per iteration instead of 8:
+//   pack   p = p * beta + r (update of the previous iteration) -> p, padded K1 operand
+//   K1     (K1-TC-sym)
+//   epi    row / column records -> Ap, its block's share of p.Ap, and in the
+//          LAST block to finish: the fixed-order sum over blocks -> step,
+//          breakdown check (solvers.py:108-113)
+//   update x += step p, r -= step Ap, block shares of r.r, LAST block:
+//          convergence / budget / beta (solvers.py:114-121)
+// "Last block": each block writes its share, fences, takes a ticket; the
+// block with the final ticket sums the shares in index order - the order
+// never depends on which block finishes last (deterministic), and the scalar
+// step needs no extra single-block launch.
+
+// fixed-order sum of one value per thread over the block (any blockDim that
+// is a multiple of 32): xor-shuffle tree per warp, then the warps in order
+__device__ double block_sum_fixed(double v, double* sm) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sm[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < nw; ++w) t += sm[w];
+  return t;  // every thread holds the block sum
+}
+
+// block `blockIdx.x` deposits `val` (thread 0) into part[], returns true in
+// the block that deposited last (which then sees every share)
+__device__ bool deposit_last(double val, double* part, unsigned* counter, int nblk) {
+  __shared__ unsigned ticket;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = val;
+    __threadfence();
+    ticket = atomicAdd(counter, 1u);
+  }
+  __syncthreads();
+  const bool last = ticket == (unsigned)nblk - 1u;
+  if (last) __threadfence();
+  return last;
+}
+
+// fixed-order sum of part[0..nblk) by one block (the shares of other blocks
+// are read through L2): threads 0..63 take every 64th share, whatever the
+// block size, so kernels of different block sizes sum in the same order
+__device__ double sum_shares(const double* part, int nblk, double* sm) {
+  double v = 0.0;
+  if (threadIdx.x < 64)
+    for (int b = threadIdx.x; b < nblk; b += 64) v += __ldcg(part + b);
+  return block_sum_fixed(v, sm);
+}
+
+__device__ void cg1_finish_pap(double pap, CgState s) {
+  if (threadIdx.x == 0 && s.active[0]) {
+    if (pap <= 0.0) {  // breakdown: operator not SPD (solvers.py:110-113)
+      *s.status = 1;
+      *s.bad_col = 0;
+      *s.done = 1;
+    }
+    s.step[0] = s.rs[0] / pap;
+  }
+}
+
+__global__ void k_cg1_pack(double* __restrict__ p, const double* __restrict__ r,
+                           double* __restrict__ vpack, long long n, long long n_pad, CgState s) {
+  if (*s.done) return;
+  const double beta = s.beta[0];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (i < n) {
+      v = __dadd_rn(__dmul_rn(p[i], beta), r[i]);  // first iteration: beta = 0, p = r = b
+      p[i] = v;
+    }
+    vpack[i] = v;
+  }
+}
+
+// k_tcsym_epilogue + the p.Ap shares + the step (one RHS, one rank)
+__global__ void __launch_bounds__(64 * kTsGroups)
+    k_tcsym_epilogue_cg(const double* __restrict__ rowpart, const double* __restrict__ colpart,
+                        const int* __restrict__ r_ptr, const int* __restrict__ r_rec,
+                        const int* __restrict__ c_ptr, const int* __restrict__ c_rec, long long n,
+                        double scale, double noise, const double* __restrict__ p,
+                        double* __restrict__ out, double* part, unsigned* counter, CgState s) {
+  __shared__ double pt[2][kTsGroups][64];
+  __shared__ double sm[32];
+  if (*s.done) return;
+  const int c = blockIdx.x;
+  const int jj = threadIdx.x & 63, g = threadIdx.x >> 6;
+  const int I = c >> 1, r = (c & 1) * 64 + jj;
+  pt[0][g][jj] = sum_records<64>(colpart, c_rec, c_ptr[c], c_ptr[c + 1], g, jj);
+  pt[1][g][jj] = sum_records<128>(rowpart, r_rec, r_ptr[I], r_ptr[I + 1], g, r);
+  __syncthreads();
+  const long long i = (long long)c * 64 + jj;
+  double d = 0.0;
+  if (g == 0 && i < n) {
+    double o = 0.0;
+#pragma unroll
+    for (int u = 0; u < kTsGroups; ++u) o += pt[0][u][jj];
+#pragma unroll
+    for (int u = 0; u < kTsGroups; ++u) o += pt[1][u][jj];
+    o = __dmul_rn(scale, o);
+    if (noise != 0.0) o = __dadd_rn(o, __dmul_rn(noise, p[i]));
+    out[i] = o;
+    d = p[i] * o;
+  }
+  const double share = block_sum_fixed(d, sm);
+  if (deposit_last(share, part, counter, (int)gridDim.x)) {
+    const double pap = sum_shares(part, (int)gridDim.x, sm);
+    cg1_finish_pap(pap, s);
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+}
+
+// p.Ap shares + the step (multi-rank CG, after the all-reduce of Ap): the
+// same 64-row blocks and in-block order as k_tcsym_epilogue_cg, so a one-rank
+// communicator reproduces the plain context bit for bit
+__global__ void __launch_bounds__(64) k_cg1_pap(const double* __restrict__ p, const double* __restrict__ ap,
+                                                long long n, double* part, unsigned* counter, CgState s) {
+  __shared__ double sm[32];
+  if (*s.done) return;
+  const long long i = (long long)blockIdx.x * 64 + threadIdx.x;
+  const double d = i < n ? p[i] * ap[i] : 0.0;
+  const double share = block_sum_fixed(d, sm);
+  if (deposit_last(share, part, counter, (int)gridDim.x)) {
+    const double pap = sum_shares(part, (int)gridDim.x, sm);
+    cg1_finish_pap(pap, s);
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_cg1_update(double* __restrict__ x, double* __restrict__ r,
+                                                    const double* __restrict__ p,
+                                                    const double* __restrict__ ap, long long n,
+                                                    double* part, unsigned* counter, int it,
+                                                    int max_iter, CgState s) {
+  __shared__ double sm[32];
+  if (*s.done) return;
+  const double st = s.step[0];
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(st, p[i]));
+    const double rv = __dsub_rn(r[i], __dmul_rn(st, ap[i]));
+    r[i] = rv;
+    acc = fma(rv, rv, acc);
+  }
+  const double share = block_sum_fixed(acc, sm);
+  if (deposit_last(share, part, counter, (int)gridDim.x)) {
+    const double rs_new = sum_shares(part, (int)gridDim.x, sm);
+    if (threadIdx.x == 0) {
+      const double nrm = sqrt(rs_new);
+      if (nrm <= s.tol[0] || it >= max_iter) {  // converged, or budget spent (reported)
+        s.iters[0] = it;
+        s.res[0] = nrm;
+        s.active[0] = 0;
+        *s.done = 1;
+      } else {
+        s.beta[0] = rs_new / s.rs[0];
+        s.rs[0] = rs_new;
+      }
+      *counter = 0u;
+    }
   }
 }
 
@@ -721,7 +912,6 @@ __global__ void k_pt_radius(const double* __restrict__ x, long long n, int d,
 // Each side's sum is split over kTsGroups thread groups (group g takes list
 // entries g, g + G, ...) and combined in g order, column side first: fixed
 // order, deterministic.
-constexpr int kTsGroups = 8;
 __global__ void __launch_bounds__(64 * kTsGroups)
     k_tcsym_epilogue(const double* __restrict__ rowpart, const double* __restrict__ colpart,
                      const int* __restrict__ r_ptr, const int* __restrict__ r_rec,
@@ -732,13 +922,9 @@ __global__ void __launch_bounds__(64 * kTsGroups)
   if (is_done(done)) return;
   const int c = blockIdx.x;
   const int jj = threadIdx.x & 63, g = threadIdx.x >> 6;
-  double s = 0.0;
-  for (int e = c_ptr[c] + g; e < c_ptr[c + 1]; e += kTsGroups) s += colpart[(size_t)c_rec[e] * 64 + jj];
-  part[0][g][jj] = s;
   const int I = c >> 1, r = (c & 1) * 64 + jj;
-  double t = 0.0;
-  for (int e = r_ptr[I] + g; e < r_ptr[I + 1]; e += kTsGroups) t += rowpart[(size_t)r_rec[e] * 128 + r];
-  part[1][g][jj] = t;
+  part[0][g][jj] = sum_records<64>(colpart, c_rec, c_ptr[c], c_ptr[c + 1], g, jj);
+  part[1][g][jj] = sum_records<128>(rowpart, r_rec, r_ptr[I], r_ptr[I + 1], g, r);
   __syncthreads();
   const long long i = (long long)c * 64 + jj;
   if (g == 0 && i < n) {
@@ -900,6 +1086,36 @@ void cg_fin_rs(Context* c, const double* part, int nblk, int t, int it, int max_
 
 void cg_update_p(Context* c, double* p, const double* r, int64_t n, int t, CgState s) {
   k_cg_update_p<<<grid_for(n * t), 256, 0, c->stream>>>(p, r, n * t, t, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void cg1_pack(Context* c, double* p, const double* r, double* vpack, int64_t n, int64_t n_pad,
+              CgState s) {
+  k_cg1_pack<<<grid_for(n_pad), 256, 0, c->stream>>>(p, r, vpack, n, n_pad, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void tcsym_epilogue_cg(Context* c, const double* rowpart, const double* colpart, const int* r_ptr,
+                       const int* r_rec, const int* c_ptr, const int* c_rec, int64_t n,
+                       double scale, double noise, const double* p, double* out, double* part,
+                       unsigned* counter, CgState s) {
+  if (n <= 0) return;
+  k_tcsym_epilogue_cg<<<(unsigned)((n + 63) / 64), 64 * kTsGroups, 0, c->stream>>>(
+      rowpart, colpart, r_ptr, r_rec, c_ptr, c_rec, n, scale, noise, p, out, part, counter, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+int cg1_blocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (n + 255) / 256)); }
+
+void cg1_pap(Context* c, const double* p, const double* ap, int64_t n, double* part,
+             unsigned* counter, CgState s) {
+  k_cg1_pap<<<(unsigned)((n + 63) / 64), 64, 0, c->stream>>>(p, ap, n, part, counter, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void cg1_update(Context* c, double* x, double* r, const double* p, const double* ap, int64_t n,
+                double* part, unsigned* counter, int it, int max_iter, CgState s) {
+  k_cg1_update<<<cg1_blocks(n), 256, 0, c->stream>>>(x, r, p, ap, n, part, counter, it, max_iter, s);
   LGP_LAUNCH_CHECK(c);
 }
 

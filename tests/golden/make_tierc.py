@@ -138,9 +138,38 @@ def cfg3():
     log("cfg3 done")
 
 
-def n50k(tag):
+def blocked_cholesky_solve_lower(a, rhs, nb=4096):
+    """In place: the lower triangle of the symmetric `a` (C order) becomes L
+    with a = L L^T (right-looking blocked Cholesky, every LAPACK / BLAS call on
+    a block of < 2^31 elements); returns L^-1 rhs."""
+    n = a.shape[0]
+    for k0 in range(0, n, nb):
+        k1 = min(n, k0 + nb)
+        a[k0:k1, k0:k1] = scipy.linalg.cholesky(a[k0:k1, k0:k1], lower=True, check_finite=False)
+        if k1 == n:
+            break
+        l11 = a[k0:k1, k0:k1]
+        # panel below the diagonal block: A21 L11^-T
+        a[k1:, k0:k1] = scipy.linalg.solve_triangular(l11, a[k1:, k0:k1].T, lower=True,
+                                                      check_finite=False).T
+        p = a[k1:, k0:k1]
+        for j0 in range(k1, n, nb):  # trailing lower triangle, block column by block column
+            j1 = min(n, j0 + nb)
+            a[j0:, j0:j1] -= p[j0 - k1:] @ p[j0 - k1:j1 - k1].T
+        log("  cholesky block", k0 // nb + 1, "of", -(-n // nb))
+    h = np.empty_like(rhs)
+    for k0 in range(0, n, nb):
+        k1 = min(n, k0 + nb)
+        t = rhs[k0:k1] - a[k0:k1, :k0] @ h[:k0]
+        h[k0:k1] = scipy.linalg.solve_triangular(a[k0:k1, k0:k1], t, lower=True, check_finite=False)
+    return h
+
+
+def n50k(tag, scratch=os.environ.get("TIERC_SCRATCH", "/tmp/tierc")):
     # SURVEY.md §8c tier C: "check the same kernel/D/t at a reduced N where the
-    # dense replay fits (N <= 50k)"
+    # dense replay fits (N <= 50k)". Resumable: each stage's result is kept in
+    # `scratch` (the CG, SLQ and Cholesky stages take minutes each).
+    os.makedirs(scratch, exist_ok=True)
     kern = {"rbf": O.CONFIGS["cfg4"]["kernel"], "m32": O.CONFIGS["cfg5"]["kernel"]}[tag]
     n, d, noise = 50000, 8, 0.1
     x, y = O.synthetic(n, d)
@@ -153,28 +182,35 @@ def n50k(tag):
     gram_y.flat[:: n + 1] += noise
     apply = lambda v: gram_y @ v  # noqa: E731
     fit_cfg = M.CgConfig(rel_tolerance=1e-8)  # models.py FIT_CG_TOLERANCE
-    log(tag, "CG")
-    res = M.cg_solve(apply, y, fit_cfg)
-    log(tag, "CG", res.iterations, res.final_residual)
-    ld = M.slq_logdet(apply, n, fit_cfg, seed=0)
-    quad = float(y @ res.x)
+    f_cg = os.path.join(scratch, f"{tag}_cg.npz")
+    if not os.path.exists(f_cg):
+        log(tag, "CG")
+        res = M.cg_solve(apply, y, fit_cfg)
+        np.savez(f_cg, it=res.iterations, res=res.final_residual, x=res.x)
+    g = np.load(f_cg)
+    it, resid, alpha = int(g["it"]), float(g["res"]), g["x"]
+    log(tag, "CG", it, resid)
+    f_slq = os.path.join(scratch, f"{tag}_slq.npz")
+    if not os.path.exists(f_slq):
+        ld = M.slq_logdet(apply, n, fit_cfg, seed=0)
+        np.savez(f_slq, ld=ld)
+    ld = float(np.load(f_slq)["ld"])
+    quad = float(y @ alpha)
     lml = -0.5 * (quad + ld + n * np.log(2 * np.pi))
     log(tag, "SLQ logdet", ld, "LML", lml)
     xs = np.random.default_rng(9).random((200, d))
     kstar = M.kernel_eval(k, x, xs)
-    mean = kstar.T @ res.x
-    log(tag, "Cholesky")
-    # the Gram is symmetric: its transpose view is Fortran-ordered, factor in place
-    c = scipy.linalg.cho_factor(gram_y.T, lower=True, overwrite_a=True, check_finite=False)
-    half = scipy.linalg.solve_triangular(c[0], kstar, lower=True, check_finite=False)
+    mean = kstar.T @ alpha
+    log(tag, "Cholesky (blocked: one LAPACK call on 50k^2 = 2.5e9 elements overflows the 32-bit "
+             "indices of scipy's OpenBLAS)")
+    half = blocked_cholesky_solve_lower(gram_y, kstar)
     var = np.maximum(M.kernel_diag(k, xs) - np.einsum("ij,ij->j", half, half), 0.0)
     np.savez_compressed(
         os.path.join(HERE, f"tierc_n50k_{tag}.npz"), kernel=kern, n=n, d=d, noise=noise,
-        it=res.iterations, res=res.final_residual, alpha=res.x, logdet=ld, lml=lml, mean=mean,
+        it=it, res=resid, alpha=alpha, logdet=ld, lml=lml, mean=mean,
         var=var, note="reference cg_solve/slq_logdet on the dense replay operator (slabs of "
                       "Kernel._gram); var by Cholesky")
     log(tag, "done")
-
 
 if __name__ == "__main__":
     for name in sys.argv[1:]:
