@@ -8,6 +8,13 @@
 * cfg4 (N = 100000, RBF, D = 8) at equal, pinned budgets through the reference's
   real matrix_free_matvec: CG after exactly 20 iterations and the Lanczos
   quadratures of 16 probes after 5 steps.
+* the cfg4 kernel (RBF 0.5, D = 8) and the cfg5 kernel (Matern-3/2 0.5, D = 8)
+  CONVERGED at N = 50000 (the largest N whose FP64 dense replay fits the build
+  container, SURVEY.md §8c tier C): gp_fit (CG, tol 1e-8) / gp_predict (200
+  test points) / log_marginal_likelihood against the reference's own
+  cg_solve / slq_logdet on the dense replay, variance against the exact
+  (Cholesky) one. Bars (north star): iterations within 3 %, alpha / mean / LML
+  within 1e-4 relative, variance within 3e-3 absolute.
 """
 
 import os
@@ -21,6 +28,11 @@ from oracle import gp_oracle as O
 
 pytestmark = pytest.mark.gpu
 
+# ~3x the measured errors of the pinned 20-iteration cfg4 CG (round 2 on the
+# B200: x relL2 9.4e-7, final residual 4.9e-8 relative)
+TIERC_CFG4_X_BAR = 3e-6
+TIERC_CFG4_RES_BAR = 1.5e-7
+
 
 @pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "fullsize_cfg2.npz")),
                     reason="fullsize_cfg2 fixture not generated")
@@ -30,7 +42,8 @@ def test_fullsize_cfg2_fit_predict_lml(gpu_ctx):
     x, y = O.synthetic(cfg["n"], cfg["d"])
     st = G.gp_fit(x, y, G.parse_kernel(cfg["kernel"]), cfg["noise"], "cg")
     it_ref = int(g["it"])
-    assert abs(st.cg_iterations - it_ref) <= max(3, 0.1 * it_ref), (st.cg_iterations, it_ref)
+    print(f"\n[fullsize cfg2] iterations {st.cg_iterations} vs reference {it_ref}")
+    assert abs(st.cg_iterations - it_ref) <= max(3, 0.03 * it_ref), (st.cg_iterations, it_ref)
     assert rel_l2(st.alpha, g["alpha"]) <= 1e-4
     xs = np.random.default_rng(9).random((200, cfg["d"]))
     mean, var = G.gp_predict(st, xs)
@@ -50,9 +63,12 @@ def test_tierc_cfg4_pinned_budgets(gpu_ctx):
     res = G.cg_solve(op, y, G.CgConfig(rel_tolerance=1e-30, max_iterations=int(g["it"])))
     assert res.iterations == int(g["it"])
     # un-converged iterates carry the FP32-entry perturbation amplified by the
-    # iteration (cf. test_cg_same_iteration_budget: 3e-3 after 25 steps at cond 2.5e3)
-    assert rel_l2(res.x, g["x"]) <= 1e-2
-    assert abs(res.final_residual - float(g["res"])) <= 1e-2 * float(g["res"])
+    # iteration; the bars are 3x the measured values (printed)
+    e_x = rel_l2(res.x, g["x"])
+    e_r = abs(res.final_residual - float(g["res"])) / float(g["res"])
+    print(f"\n[tier C cfg4, 20 pinned CG iterations] x relL2 {e_x:.2e}, residual rel {e_r:.2e}")
+    assert e_x <= TIERC_CFG4_X_BAR
+    assert e_r <= TIERC_CFG4_RES_BAR
     steps, probes = int(g["steps"]), int(g["probes"])
     z = G.probe_block(cfg["n"], probes, 0)
     al, be, cnt = op.lanczos(z, steps)
@@ -85,3 +101,30 @@ def test_tierc_cfg3_pinned_budgets(gpu_ctx):
         m = int(cnt[c])
         q = G.solvers.gauss_quadrature(al[c, :m], be[c, :m - 1])
         assert abs(q - g["quads"][c]) <= 1e-5 * abs(g["quads"][c]), (c, q, g["quads"][c])
+
+
+@pytest.mark.parametrize("tag", ["rbf", "m32"])
+def test_tierc_n50k_converged_fit_predict_lml(gpu_ctx, tag):
+    path = os.path.join(GOLDEN, f"tierc_n50k_{tag}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    g = golden(f"tierc_n50k_{tag}.npz")
+    n, d, noise = int(g["n"]), int(g["d"]), float(g["noise"])
+    x, y = O.synthetic(n, d)
+    st = G.gp_fit(x, y, G.parse_kernel(str(g["kernel"])), noise, "cg")
+    it_ref = int(g["it"])
+    e_alpha = rel_l2(st.alpha, g["alpha"])
+    xs = np.random.default_rng(9).random((200, d))
+    mean, var = G.gp_predict(st, xs)
+    e_mean = rel_l2(mean, g["mean"])
+    e_var = float(np.max(np.abs(var - g["var"])))
+    lml = G.log_marginal_likelihood(st, seed=0)
+    e_lml = abs(lml - float(g["lml"])) / abs(float(g["lml"]))
+    print(f"\n[tier C n50k {tag}] iterations {st.cg_iterations} vs reference {it_ref}; "
+          f"alpha relL2 {e_alpha:.2e}, mean relL2 {e_mean:.2e}, var max abs {e_var:.2e}, "
+          f"LML rel {e_lml:.2e}")
+    assert abs(st.cg_iterations - it_ref) <= 0.03 * it_ref, (st.cg_iterations, it_ref)
+    assert e_alpha <= 1e-4
+    assert e_mean <= 1e-4
+    assert e_var <= 3e-3
+    assert e_lml <= 1e-4, (lml, float(g["lml"]))

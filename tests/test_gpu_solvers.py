@@ -12,6 +12,7 @@ import pytest
 import paper_2605_17898_b200 as G
 from conftest import GOLDEN, golden, rel_l2
 from oracle import gp_oracle as O
+from paper_2605_17898_b200 import _lib
 
 pytestmark = pytest.mark.gpu
 
@@ -31,7 +32,8 @@ def test_cg_golden(gpu_ctx):
         op = G.KernelOperator(k, x, 0.1)
         res = G.cg_solve(op, b, G.CgConfig(rel_tolerance=tol))
         it_ref = int(g[f"it_{ci}"])
-        assert abs(res.iterations - it_ref) <= max(2, 0.15 * it_ref), (res.iterations, it_ref)
+        print(f"\n[cg_small case {ci}] iterations {res.iterations} vs reference {it_ref}")
+        assert abs(res.iterations - it_ref) <= max(2, 0.03 * it_ref), (res.iterations, it_ref)
         assert res.final_residual <= tol * np.linalg.norm(b) or res.iterations == min(n, 1000)
         # solution vs the reference's solution
         assert rel_l2(res.x, g[f"x_{ci}"]) <= 1e-4
@@ -49,13 +51,15 @@ def test_cg_same_iteration_budget(gpu_ctx):
     # un-converged iterates amplify the ~1e-7 FP32-entry perturbation with
     # every step: a CPU emulation (FP64 CG on the FP32-rounded Gram of this
     # system, cond ~2.5e3) drifts 1.4e-7 from the FP64 iterate after 5 steps and
-    # 3.0e-3 after 25 (a mere FP64 re-ordering: 2e-5). The converged-solution
-    # bar (1e-4) is checked in test_cg_golden.
-    for it, bar in ((5, 1e-5), (25, 1e-2)):
+    # 3.0e-3 after 25 (a mere FP64 re-ordering: 2e-5); the device measures
+    # 4.6e-7 / 2.7e-5 (round 2), bars ~3x that. The converged-solution bar
+    # (1e-4) is checked in test_cg_golden.
+    for it, bar in ((5, 1.5e-6), (25, 1e-4)):
         cfg = G.CgConfig(rel_tolerance=1e-30, max_iterations=it)
         res = G.cg_solve(G.KernelOperator(k, x, 0.1), b, cfg)
         ref = O.cg(lambda v: O.matvec(nodes, x, 0.1, v), b, 1e-30, it)
         assert res.iterations == it == ref[1]
+        print(f"\n[pinned budget {it}] x relL2 {rel_l2(res.x, ref[0]):.2e}")
         assert rel_l2(res.x, ref[0]) <= bar
 
 
@@ -119,7 +123,8 @@ def test_model_small_matrix_free_branch(gpu_ctx, name):
     xs = np.random.default_rng(9).random((8, cfg["d"]))
     st = G.gp_fit(x, y, G.parse_kernel(cfg["kernel"]), cfg["noise"], "cg")
     it_ref = int(g[f"{name}_it"])
-    assert abs(st.cg_iterations - it_ref) <= max(3, 0.1 * it_ref)
+    print(f"\n[model_small {name}] iterations {st.cg_iterations} vs reference {it_ref}")
+    assert abs(st.cg_iterations - it_ref) <= max(3, 0.03 * it_ref)
     mean, var = G.gp_predict(st, xs)
     assert rel_l2(mean, g[f"{name}_mean"]) <= 1e-4
     assert np.max(np.abs(var - g[f"{name}_var"])) <= 3e-3
@@ -127,29 +132,27 @@ def test_model_small_matrix_free_branch(gpu_ctx, name):
     assert abs(lml - float(g[f"{name}_lml"])) <= 1e-4 * abs(float(g[f"{name}_lml"]))
 
 
-@pytest.mark.parametrize("nwg,layout,xpose", [("4", "1", "1"), ("3", "1", "1"), ("2", "1", "1"),
-                                               ("4", "1", "0"), ("4", "0", "0")])
-def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg, layout, xpose):
+@pytest.mark.parametrize("nwg,r", [("4", ""), ("3", ""), ("4", "1"), ("4", "3")])
+def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg, r):
     """The symmetric tensor-core CG matvec (default for D >= 4 r^2 trees)
     evaluates each unordered pair once: exactly symmetric, so CG matches the
     symmetric SIMT kernel's (LGP_NO_TCSYM) iteration count and solution, and
-    the matvec meets the 1e-5 bar, for every epilogue warpgroup count and
-    both TMEM read layouts (1: 16x256b tiles, 0: 32x32b rows) and both column
-    reductions (shared-memory transpose, butterfly)."""
+    the matvec meets the 1e-5 bar, for 4 and 3 epilogue warpgroups and forced
+    super-tile sizes (LGP_TS_R; default: the scheduling model's choice)."""
     x, b = small_inputs(3000, 8, 41)
     k = G.parse_kernel("(scale 1.2 (rbf 0.6))")
     monkeypatch.setenv("LGP_NO_TCSYM", "1")
     base = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
     monkeypatch.delenv("LGP_NO_TCSYM")
     monkeypatch.setenv("LGP_TS_NWG", nwg)
-    monkeypatch.setenv("LGP_TS_LAYOUT", layout)
-    monkeypatch.setenv("LGP_TS_XPOSE", xpose)
-    op = G.KernelOperator(k, x, 0.1)
+    if r:
+        monkeypatch.setenv("LGP_TS_R", r)
+    op = G.KernelOperator(k, x, 0.1, ctx=_lib.Context(0))
     res = G.cg_solve(op, b, G.CgConfig(rel_tolerance=1e-8))
-    # rounding-order differences move the count either way (215 vs 222 seen
-    # for layout 1); an asymmetric operator would cost 25-50 % MORE iterations
-    assert res.iterations <= base.iterations + max(2, 0.03 * base.iterations)
-    assert res.iterations >= 0.9 * base.iterations
+    print(f"\n[tcsym nwg={nwg} R={r or 'auto'}] iterations {res.iterations} vs SIMT-sym {base.iterations}")
+    # rounding-order differences move the count either way; an asymmetric
+    # operator would cost 25-50 % MORE iterations
+    assert abs(res.iterations - base.iterations) <= max(2, 0.03 * base.iterations)
     assert rel_l2(res.x, base.x) <= 1e-4
     v = np.random.default_rng(5).standard_normal(3000)
     ref = O.matvec(O.parse_tree(G.format_kernel(k)), x, 0.1, v)
