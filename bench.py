@@ -46,8 +46,18 @@ METRIC = "kernel-matvec Gentries/s and CG solve time at N=100k, D=8, 1/2/4/8 B20
 UNIT = "Gentries/s"
 SM_COUNT = 148
 FP32_LANES = 128
-SFU_PER_SM = 16
-TMEM_LD_B_PER_CLK = 40.8  # measured tcgen05.ld throughput per SM (tools/tmem_bench.cu)
+SFU_PER_SM = 16  # MUFU.EX2 per clock per SM: tools/alu_bench.cu measures 15.96, ncu
+                 # sm__inst_executed_pipe_xu 99.6 % (profiles/r02_alu_mufu_ncu.txt)
+
+
+DTYPE_TC = ("f32 kernel entries from an FP16x2-split tcgen05 distance GEMM (FP32 accumulate) and "
+            "MUFU exp2; contraction on tcgen05 with FP16 hi/lo entries x FP16 hi/lo V (power-of-two "
+            "column scaling), FP32 TMEM accumulation over 1024-column groups, f64 sums")
+
+
+def tc_rhs_per_pass(t):
+    """Right-hand sides per K1-TC pass (lgp_codegen.cpp make_tc_plan)."""
+    return 8 if t <= 8 else (16 if t <= 16 else 32)
 
 
 def flops_per_entry(kernel_expr, d, t):
@@ -169,9 +179,33 @@ def max_over_ranks(ctx, value):
     return ctx.allreduce_max([value])[0]
 
 
-def cpu_baseline(cfg, x, seconds=12.0):
+def host_info():
+    """CPU model, core count and the BLAS thread pools (threadpoolctl)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    pools = []
+    try:
+        import threadpoolctl
+
+        pools = [{"api": i.get("internal_api"), "version": i.get("version"),
+                  "num_threads": i.get("num_threads")} for i in threadpoolctl.threadpool_info()]
+    except Exception:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "threadpools": pools}
+
+
+def cpu_baseline(cfg, x, seconds=12.0, cg_iterations=None):
     """Oracle port of the reference matvec (block=32 fit path, one RHS column)
-    on a row subset of the same workload; extrapolated as entries/s."""
+    on a row subset of the same workload; extrapolated as entries/s, and the
+    CPU CG solve time extrapolated as (time of one full matvec) x iterations
+    (SURVEY.md §8d)."""
     from oracle import gp_oracle as O
 
     nodes = O.parse_tree(cfg["kernel"])
@@ -185,17 +219,20 @@ def cpu_baseline(cfg, x, seconds=12.0):
         elapsed += time.perf_counter() - t0
         done += rows * cfg["n"]
         reps += 1
-    try:
-        import threadpoolctl
-
-        threads = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] or [1])
-    except Exception:
-        threads = os.cpu_count()
-    return {"value": done / elapsed / 1e9, "unit": UNIT, "cores": int(threads),
-            "kind": "port",
-            "sample": f"{reps} x {rows}-row slabs x all {cfg['n']} columns, t=1 (reference has no "
-                      f"multi-RHS path: t columns cost t x), block=32, FP64 NumPy/OpenBLAS "
-                      f"({threads} BLAS threads, ufuncs single-threaded), {elapsed:.1f} s"}
+    info = host_info()
+    threads = max([p["num_threads"] or 1 for p in info["threadpools"]] or [os.cpu_count() or 1])
+    rate = done / elapsed  # entries / s, one RHS column
+    out = {"value": rate / 1e9, "unit": UNIT, "cores": int(threads), "kind": "port",
+           "sample": f"{reps} x {rows}-row slabs x all {cfg['n']} columns, t=1 (reference has no "
+                     f"multi-RHS path: t columns cost t x), block=32, FP64 NumPy/OpenBLAS "
+                     f"({threads} BLAS threads, ufuncs single-threaded), {elapsed:.1f} s",
+           "matvec_s_extrapolated": cfg["n"] ** 2 / rate}
+    out.update(info)
+    if cg_iterations:
+        out["cg_solve_s_extrapolated"] = cg_iterations * cfg["n"] ** 2 / rate
+        out["cg_solve_note"] = (f"one full reference matvec ({cfg['n'] ** 2 / rate:.1f} s) x the "
+                                f"{cg_iterations} iterations of the device solve")
+    return out
 
 
 def run_reference(args, rank, world):
@@ -227,12 +264,8 @@ def run_reference(args, rank, world):
             times.append(dt)
     total = sum(times)
     value = args.steps * rows * cfg["n"] * t / total / 1e9
-    try:
-        import threadpoolctl
-
-        threads = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] or [1])
-    except Exception:
-        threads = os.cpu_count()
+    info = host_info()
+    threads = max([p["num_threads"] or 1 for p in info["threadpools"]] or [os.cpu_count() or 1])
     sample = (f"per step: {rows}-row slab of the {cfg['n']}x{cfg['n']} operator x {t} RHS columns "
               f"(each column a separate reference matvec, block=32)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
@@ -240,8 +273,8 @@ def run_reference(args, rank, world):
             "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args.config, cfg),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(threads), "kind": "port",
-                             "sample": sample},
+            "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": int(threads), "kind": "port",
+                                  "sample": sample}, **info),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -327,14 +360,11 @@ def run_ours(args, rank, world):
                     row_range=(r0, r0 + 64))
     parity = float(np.linalg.norm(out[r0:r0 + 64, :2] - want) / np.linalg.norm(want))
 
-    # e2e: public API call with pinned host buffers (H2D of X, V; D2H of the product)
-    hx, hv = C.c_void_p(), C.c_void_p()
-    _lib.check(lib.lgp_host_alloc(x.nbytes, C.byref(hx)))
-    _lib.check(lib.lgp_host_alloc(z.nbytes, C.byref(hv)))
-    px = np.ctypeslib.as_array(C.cast(hx, C.POINTER(C.c_double)), shape=x.shape)
-    pv = np.ctypeslib.as_array(C.cast(hv, C.POINTER(C.c_double)), shape=z.shape)
-    px[...] = x
-    pv[...] = z
+    # e2e: the public API call exactly as a NumPy caller makes it - ordinary
+    # (pageable) NumPy arrays X, V in, a NumPy array out: H2D of X and V and
+    # D2H of the product inside the timed region
+    px = np.array(x, copy=True)
+    pv = np.array(z, copy=True)
     # warm-up in the timed loop's own pattern (the previous result stays alive
     # while the next call runs), so pooled host/device buffers are in place; the
     # host-side call time settles over ~20-30 calls on the gpurun boxes
@@ -351,7 +381,7 @@ def run_ours(args, rank, world):
     del res
     e2e = {"value": n * n * t * e2e_steps / e2e_s / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": int(x.nbytes + z.nbytes), "d2h_bytes_per_step": int(z.nbytes),
-           "ms_per_step": e2e_s / e2e_steps * 1e3,
+           "ms_per_step": e2e_s / e2e_steps * 1e3, "host_buffers": "pageable NumPy arrays",
            "path": "paper_2605_17898_b200.matrix_free_matvec(kernel, X, noise, V) -> lgp_matvec"}
 
     # CG solve (alpha) and SLQ log-det through the device solver loops
@@ -394,36 +424,37 @@ def run_ours(args, rank, world):
             traffic = json.load(f).get(args.config)
     except Exception:
         pass
-    tc = "lgp_matvec_tc" in prog.source(d, t)
-    sfu_frac = rows_local * n * sfu / (k1_avg_ms * 1e-3) / (SFU_PER_SM * SM_COUNT * f_mhz * 1e6)
+    tc = "lgp_matvec_tc(" in prog.source(d, t)
+    sfu_peak = SFU_PER_SM * SM_COUNT * f_mhz * 1e6 / 1e12  # T op/s
+    # algorithmic SFU ops per launch: one per kernel entry
+    # (K1-TC re-evaluates the entries per pass of <= 32 RHS: t <= 32 is one pass)
+    sfu_ach = rows_local * n * sfu / (k1_avg_ms * 1e-3) / 1e12
+    bf16 = float(pk.get("bf16_tflops", 1648.7))
     if tc:
-        # K1-TC's binding resource is the TMEM -> register path: every kernel
-        # entry's FP32 -r^2 is read once by tcgen05.ld (4 B / entry / pass).
-        # Peak = measured tcgen05.ld throughput, 40.8 B/clk/SM on this B200
-        # (tools/tmem_bench.cu, flat in shape and warp count), x 148 SMs x clock.
-        n_pass = -(-t // 16)
-        tmem_bytes = rows_local * n * 4 * n_pass
-        tmem_peak = TMEM_LD_B_PER_CLK * SM_COUNT * f_mhz * 1e6 / 1e9  # GB/s
-        tmem_ach = tmem_bytes / (k1_avg_ms * 1e-3) / 1e9
-        # tensor-core work: distance GEMM (K = 3D+4 rounded to 16) + contraction
-        # (K = 2 x 64 per chunk, N = 32) over 128 x 64 chunks
+        # K1-TC: per 128 x 64 chunk the distance GEMM (K = 3D+4 rounded to 16)
+        # and the contraction (K = 2 x 64, N = 2 x RHS per pass) on tcgen05
+        n_pass = -(-t // tc_rhs_per_pass(t))
         kh = -(-(3 * d + 4) // 16) * 16
         chunks = -(-rows_local // 128) * -(-n // 64) * n_pass
-        tflop = chunks * (2 * 128 * 64 * kh + 2 * 128 * 32 * 128) / (k1_avg_ms * 1e-3) / 1e12
-        roofline = {"bound": "tensor", "achieved": tmem_ach, "peak": tmem_peak, "unit": "GB/s",
-                    "frac": tmem_ach / tmem_peak, "traffic": traffic,
+        tflop = chunks * (2 * 128 * 64 * kh + 2 * 128 * (2 * tc_rhs_per_pass(t)) * 128) \
+            / (k1_avg_ms * 1e-3) / 1e12
+        roofline = {"bound": "sfu", "achieved": sfu_ach, "peak": sfu_peak, "unit": "T SFU op/s",
+                    "frac": sfu_ach / sfu_peak, "traffic": traffic,
                     "kernel": "lgp_matvec_tc (fused K1: tcgen05 FP16x2 distance GEMM -> TMEM -> "
                               "exp2 epilogue -> FP16 hi/lo contraction GEMM)",
                     "k1_ms_per_launch": k1_avg_ms,
-                    "resource": "tensor-memory loads (tcgen05.ld of the FP32 distance tile), "
-                                "4 B per kernel entry",
-                    "peak_source": f"measured tcgen05.ld {TMEM_LD_B_PER_CLK} B/clk/SM "
-                                   f"(tools/tmem_bench.cu) x {SM_COUNT} SMs x {f_mhz:.0f} MHz",
-                    "tensor_tflops": tflop,
-                    "tensor_frac_of_bf16_dense": tflop / float(pk.get("bf16_tflops", 1652.9)),
-                    "sfu_frac": sfu_frac,
-                    "fp32_equivalent_tflops": achieved,
-                    "hbm_frac": (traffic / (k1_avg_ms * 1e-3) / 1e9 / float(pk.get("hbm_gbs", 6449.1))
+                    "resource": "the special-function unit: one exp2 per kernel entry (SURVEY.md "
+                                "§8d: 1 SFU op per RBF entry), MUFU.EX2 at 16/clk/SM",
+                    "peak_source": f"{SFU_PER_SM} MUFU.EX2/clk/SM x {SM_COUNT} SMs x {f_mhz:.0f} MHz: "
+                                   "tools/alu_bench.cu measures 15.96/clk/SM at ncu "
+                                   "sm__inst_executed_pipe_xu 99.6 %; K1-TC runs that pipe at 61.7 % "
+                                   "(profiles/r02_k1tc_t16_ncu_summary.txt)",
+                    "tensor": {"issued_tflops": tflop, "peak_measured_bf16_tflops": bf16,
+                               "frac": tflop / bf16},
+                    "algorithmic_fp32": {"flops_per_entry": flops, "tflops": achieved,
+                                         "frac_of_measured_bf16": achieved / bf16,
+                                         "frac_of_fp32_simt_peak": achieved / fp32_peak},
+                    "hbm_frac": (traffic / (k1_avg_ms * 1e-3) / 1e9 / float(pk.get("hbm_gbs", 6444.7))
                                  if traffic else None)}
     else:
         roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
@@ -433,20 +464,21 @@ def run_ours(args, rank, world):
                     "flops_per_entry": flops, "sfu_per_entry": sfu,
                     "peak_source": f"derived: 2 x {FP32_LANES} FP32 lanes x {SM_COUNT} SMs x "
                                    f"{f_mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)",
-                    "sfu_frac": sfu_frac}
+                    "sfu_frac": sfu_ach / sfu_peak}
         if clk.get("sm_mhz"):
             roofline["frac_at_observed_clock"] = achieved / (fp32_peak * clk["sm_mhz"] / f_mhz)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 entries / f64 accumulate", "data": "synthetic",
+            "dtype": DTYPE_TC if tc else "f32 entries, f64 accumulation (SIMT)", "data": "synthetic",
             "config": workload_config(args.config, cfg, world, args.sharded),
             "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "parity_rel_l2": parity}
     line.update(solve)
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, x)
+        line["cpu_baseline"] = cpu_baseline(
+            cfg, x, cg_iterations=solve.get("cg_solve", {}).get("iterations"))
     print(json.dumps(line), flush=True)
     return 0
 

@@ -1,11 +1,13 @@
 // JIT skeleton of the tensor-core fused matvec (K1-TC) for kernel trees whose
-// leaves are all functions of r^2 (RBF / Matern-3/2 / Matern-5/2, with Scale,
-// Sum, Product), D >= 4.
+// leaves are functions of r^2 (RBF / Matern-3/2 / Matern-5/2) or Periodic
+// (angle addition on per-point features), with Scale / Sum / Product.
 //
 // Prepended by lgp_codegen.cpp: lgp_jit_abi.h, #defines LGP_D, LGP_TC_KD
 // (K of the distance GEMM in FP16 halves: 3D + 4 rounded up to 16), LGP_TC_N
-// (RHS per pass, 16), LGP_TC_G (chunks per FP32 accumulation group),
-// LGP_TC_STAGES, and the generated lgp_tc_prep_point() / lgp_tc_k().
+// (right-hand sides per pass: 8, 16 or 32), LGP_TC_NSB (S buffers that fit
+// next to the accumulators in TMEM), LGP_TC_G (chunks per FP32 accumulation
+// group), LGP_TC_STAGES, LGP_TC_FW / P0 / PF (FP32 point features, Periodic
+// block), and the generated lgp_tc_prep_point() / lgp_tc_k() / lgp_tc_kf().
 //
 // Per CTA: 128 rows (one TMEM lane each) x one column segment, streamed in
 // 64-column chunks.
@@ -25,33 +27,23 @@
 //   registers; the two epilogue warpgroups' FP64 sums are combined in a fixed
 //   order and written as this segment's partial (deterministic).
 //
-// Warp roles: warp 0 = TMA bulk-copy producer (+ TMEM allocator), warp 1 =
-// MMA issuer (one thread, polling: the distance GEMM runs up to 4 chunks ahead
-// of the contraction), warps 2..5 / 6..9 = epilogue warpgroups 0 / 1 (even /
-// odd chunks). TMEM: 4 S buffers of 64 columns (S' in FP32, then P packed
-// FP16 hi | lo in place) + 2x2 D2 accumulators.
+// Warp roles: warp 0 = TMA bulk-copy producer (+ TMEM allocator), warp 11 =
+// distance-GEMM issuer, warps 1 / 10 = contraction issuers of epilogue
+// warpgroups 0 / 1 (one MMA-issuing thread sustains ~60-90 cycles per MMA),
+// warps 2..5 / 6..9 = epilogue warpgroups 0 / 1 (even / odd chunks). TMEM:
+// LGP_TC_NSB S buffers of 64 columns (S' in FP32, then P packed FP16 hi | lo
+// in place) + 2 x 2 D2 accumulators of 2N columns.
+//
+// (Measured and dropped, round 1: CTA pairs (cta_group::2, M = 256: 5.1 vs
+// 3.6 ms at cfg4 - MMA instructions are not the binding resource), distance
+// tiles on mma.sync (4.2-5.3 ms), distance tiles on the FMA pipe (4.4-5.0 ms),
+// 3-4 epilogue warpgroups with shared-memory row sums (4.6 ms).)
 
-#ifdef LGP_TC_TRACE
-#define TR_DECL unsigned long long tr_t = clock64(); unsigned long long tr_acc[12] = {0,0,0,0,0,0,0,0,0,0,0,0};
-#define TR_MARK(slot) { const unsigned long long n_ = clock64(); tr_acc[slot] += n_ - tr_t; tr_t = n_; }
-#define TR_FLUSH(lo, hi) { for (int q_ = lo; q_ <= hi; ++q_) atomicAdd(a.trace + q_, tr_acc[q_]); }
-#else
-#define TR_FLUSH(lo, hi)
-#define TR_DECL
-#define TR_MARK(slot)
-#endif
-
-#ifndef LGP_TC_PRIO
-#define LGP_TC_PRIO 1
-#endif
 #ifndef LGP_TC_DLAG
 #define LGP_TC_DLAG ((LGP_TC_G + 1) / 2)
 #endif
 #if LGP_TC_DLAG < 1 || LGP_TC_DLAG > LGP_TC_G
 #error "LGP_TC_DLAG must be in [1, LGP_TC_G]"
-#endif
-#ifndef LGP_TC_ABLATE
-#define LGP_TC_ABLATE 0
 #endif
 // S' = -r^2 may come out a rounding error above 0; leaves that take sqrt(r^2)
 // need it clamped (LGP_TC_CLAMP defined by the code generator), exp2 does not
@@ -59,11 +51,10 @@
 #define LGP_TC_CLAMP(x) (x)
 #endif
 
-
 #define TC_CH 64
-#define TC_THREADS 384  // 12 warps: producer, 3 MMA issuers (leader) / relay (peer), 2 epilogue warpgroups
-#if LGP_TC_N != 16
-#error "K1-TC is specialised for 16 RHS per pass"
+#define TC_THREADS 384  // 12 warps: producer, 3 MMA issuers, 2 epilogue warpgroups
+#if LGP_TC_N != 8 && LGP_TC_N != 16 && LGP_TC_N != 32
+#error "K1-TC takes 8, 16 or 32 right-hand sides per pass"
 #endif
 #define TC_N2 (2 * LGP_TC_N)  // GEMM2 N: V_hi and V_lo rows side by side
 #define TC_V_HALFS (LGP_TC_N * TC_CH)
@@ -71,46 +62,13 @@
 #define TC_A1_BYTES (128 * LGP_TC_KD * 2)
 #define TC_B1_BYTES (TC_CH * LGP_TC_KD * 2)
 #define TC_V_BYTES (2 * TC_V_HALFS * 2)
-// a CTA pair splits every chunk's B operands along N: rank r stages columns
-// 32r..32r+31 of the column features and V_hi (r = 0) or V_lo (r = 1)
-#ifndef LGP_TC_PAIR
-#define LGP_TC_PAIR 0
-#endif
-#if LGP_TC_PAIR
-#define TC_CG "2"
-#define TC_M 256
-#define TC_B1H_BYTES (TC_B1_BYTES / 2)
-#define TC_VH_BYTES (TC_V_BYTES / 2)
-#else
-#define TC_CG "1"
-#define TC_M 128
-#define TC_B1H_BYTES TC_B1_BYTES
-#define TC_VH_BYTES TC_V_BYTES
-#endif
-#define TC_NEPI (4 * (1 + LGP_TC_PAIR))  // epilogue warps arriving on PFULL / D2EMPTY
-// chunks c with bit (c % 8) set compute -r^2 on the FMA pipe from FP32
-// features instead of the distance GEMM: they need no tcgen05.ld, the K1-TC
-// roofline resource, at the cost of D + 1 FMAs and D/4 + 1 broadcast loads per
-// entry. Opt-in (LGP_TC_SIMT_MASK): measured slower on cfg4 (1 of 8 chunks:
-// 4.44 ms, 2 of 8: 4.96 ms vs 3.69 ms) - with two epilogue warps per SM
-// sub-partition the FMA chain cannot hide its latency.
-#ifndef LGP_TC_SIMT_MASK
-#define LGP_TC_SIMT_MASK 0
-#endif
 #ifndef LGP_TC_PF
 #define LGP_TC_PF 0  // Periodic (cos, sin) features per point, from offset LGP_TC_P0
 #define LGP_TC_P0 0
 #endif
-// FP32 column features of a chunk (staged for FMA-pipe distance chunks, and
-// for every chunk when the tree has Periodic leaves)
-#define TC_C32_BYTES ((LGP_TC_SIMT_MASK || LGP_TC_PF) ? TC_CH * LGP_TC_FW * 4 : 0)
-#define TC_C32(c) (TC_SIMT(c) || LGP_TC_PF > 0)
-#define TC_STAGE_BYTES (TC_B1H_BYTES + TC_VH_BYTES + TC_C32_BYTES)
-#if LGP_TC_PAIR && LGP_TC_SIMT_MASK
-#error "FMA-pipe distance chunks are single-CTA only"
-#endif
-#define TC_SIMT(c) ((LGP_TC_SIMT_MASK >> ((c) & 7)) & 1)
-#define TC_HMMA_CHUNK(c) ((LGP_TC_HMMA >> ((c) & 7)) & 1)
+// FP32 column features of a chunk (trees with Periodic leaves)
+#define TC_C32_BYTES (LGP_TC_PF ? TC_CH * LGP_TC_FW * 4 : 0)
+#define TC_STAGE_BYTES (TC_B1_BYTES + TC_V_BYTES + TC_C32_BYTES)
 #define TC_COMB_BYTES (128 * LGP_TC_N * 8)
 #ifndef LGP_TC_NSB
 #define LGP_TC_NSB 6   // S buffers in TMEM (64 columns each), even: NSB/2 per warpgroup
@@ -119,21 +77,17 @@
 #if 64 * LGP_TC_NSB + 4 * TC_N2 > 512
 #error "TMEM budget: S buffers + 2x2 D2 accumulators exceed 512 columns"
 #endif
-#define TC_NBARS (10 + 3 * LGP_TC_STAGES + 3 * LGP_TC_NSB)
+#define TC_NBARS (1 + 2 * LGP_TC_STAGES + 3 * LGP_TC_NSB + 8)
 
 // barrier slots
-// (P* = arrivals relayed from the peer CTA; PFULL / D2EMPTY count the
-// epilogue warps of both CTAs; the rest are local)
 #define B_AFULL 0
-#define B_PAFULL 1
-#define B_SFULL(s) (2 + (s))
-#define B_SEMPTY(s) (2 + LGP_TC_STAGES + (s))
-#define B_PSFULL(s) (2 + 2 * LGP_TC_STAGES + (s))
-#define B_S1FULL(q) (2 + 3 * LGP_TC_STAGES + (q))
-#define B_PFULL(q) (2 + 3 * LGP_TC_STAGES + LGP_TC_NSB + (q))
-#define B_D2FULL(w, b) (2 + 3 * LGP_TC_STAGES + 2 * LGP_TC_NSB + 2 * (w) + (b))
-#define B_D2EMPTY(w, b) (6 + 3 * LGP_TC_STAGES + 2 * LGP_TC_NSB + 2 * (w) + (b))
-#define B_PEMPTY(q) (10 + 3 * LGP_TC_STAGES + 2 * LGP_TC_NSB + (q))
+#define B_SFULL(s) (1 + (s))
+#define B_SEMPTY(s) (1 + LGP_TC_STAGES + (s))
+#define B_S1FULL(q) (1 + 2 * LGP_TC_STAGES + (q))
+#define B_PFULL(q) (1 + 2 * LGP_TC_STAGES + LGP_TC_NSB + (q))
+#define B_PEMPTY(q) (1 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB + (q))
+#define B_D2FULL(w, b) (1 + 2 * LGP_TC_STAGES + 3 * LGP_TC_NSB + 2 * (w) + (b))
+#define B_D2EMPTY(w, b) (5 + 2 * LGP_TC_STAGES + 3 * LGP_TC_NSB + 2 * (w) + (b))
 
 // blocking mbarrier waits let the hardware suspend the waiting thread (up to
 // this many ns per try) instead of spinning: spinning producer / issuer /
@@ -212,66 +166,10 @@ __device__ __forceinline__ bool lgp_mbar_test(unsigned bar, unsigned parity) {
 
 __device__ __forceinline__ void lgp_mbar_wait(unsigned bar, unsigned parity) {
   unsigned ok = 0;
-#ifdef LGP_TC_WATCHDOG
-  unsigned long long spins = 0;
-#endif
   while (!ok) {
-#ifdef LGP_TC_WATCHDOG
-    if (++spins > (1ull << 28)) asm volatile("trap;");
-#endif
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity), "r"(LGP_TC_SUSPEND_NS)
-        : "memory");
-  }
-}
-
-// ---- CTA-pair (cluster of 2) helpers
-__device__ __forceinline__ unsigned lgp_cluster_rank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void lgp_cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-// address of this CTA's shared variable `a` in the shared window of CTA `rank`
-__device__ __forceinline__ unsigned lgp_mapa(unsigned a, unsigned rank) {
-  unsigned r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void lgp_mbar_arrive_cluster(unsigned cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-__device__ __forceinline__ bool lgp_mbar_test_cl(unsigned bar, unsigned parity) {
-  unsigned ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void lgp_mbar_wait_cl(unsigned bar, unsigned parity) {
-  unsigned ok = 0;
-#ifdef LGP_TC_WATCHDOG
-  unsigned long long spins = 0;
-#endif
-  while (!ok) {
-#ifdef LGP_TC_WATCHDOG
-    if (++spins > (1ull << 28)) asm volatile("trap;");
-#endif
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(bar), "r"(parity), "r"(LGP_TC_SUSPEND_NS)
@@ -296,15 +194,12 @@ __device__ __forceinline__ unsigned long long lgp_sdesc(unsigned saddr, unsigned
          ((unsigned long long)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-// cta_group::2: issued by the pair's leader (rank 0); M = 256 rows, rows
-// 0..127 from / into the leader's SMEM / TMEM, 128..255 the peer's; B rows
-// 0..N/2-1 from the leader's SMEM, N/2..N-1 from the peer's (same offsets)
 __device__ __forceinline__ void lgp_mma_f16_ss(unsigned d, unsigned long long ad,
                                                unsigned long long bd, unsigned idesc,
                                                unsigned acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::" TC_CG ".kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
 
@@ -312,42 +207,15 @@ __device__ __forceinline__ void lgp_mma_f16_ts(unsigned d, unsigned a_tmem, unsi
                                                unsigned idesc, unsigned acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::" TC_CG ".kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a_tmem), "l"(bd), "r"(idesc), "r"(acc));
 }
 
-#if LGP_TC_PAIR
-// completion of the pair's MMAs, signalled on the leader's barrier only
-__device__ __forceinline__ void lgp_mma_commit_local(unsigned bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;" ::"r"(bar),
-      "h"((unsigned short)1)
-      : "memory");
-}
-// completion of the pair's MMAs, signalled on the barrier at this offset in both CTAs
-__device__ __forceinline__ void lgp_mma_commit(unsigned bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;" ::"r"(bar),
-      "h"((unsigned short)3)
-      : "memory");
-}
-// epilogue -> leader barrier
-__device__ __forceinline__ void lgp_arrive_leader(unsigned bar) {
-  lgp_mbar_arrive_cluster(lgp_mapa(bar, 0));
-}
-#define lgp_mbar_wait_ld lgp_mbar_wait_cl
-#else
 __device__ __forceinline__ void lgp_mma_commit(unsigned bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    bar)
                : "memory");
 }
-#define lgp_mma_commit_local lgp_mma_commit
-#define lgp_arrive_leader lgp_mbar_arrive
-#define lgp_mbar_wait_ld lgp_mbar_wait
-#endif
 
 __device__ __forceinline__ void lgp_tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -411,38 +279,10 @@ __device__ __forceinline__ void lgp_tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// ---- warp-level tensor-core distance tile (LGP_TC_HMMA): mma.sync keeps -r^2
-// in registers, so no tcgen05.ld of an FP32 S tile is needed
-// LGP_TC_HMMA: mask over c % 8 of the chunks that take this path (0xFF = all)
-#ifndef LGP_TC_HMMA
-#define LGP_TC_HMMA 0
-#endif
-__device__ __forceinline__ void lgp_ldsm_x4(unsigned addr, unsigned (&r)[4]) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(addr));
-}
-__device__ __forceinline__ void lgp_ldsm_x2(unsigned addr, unsigned& r0, unsigned& r1) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
-               : "=r"(r0), "=r"(r1)
-               : "r"(addr));
-}
-__device__ __forceinline__ void lgp_hmma(float (&c)[4], const unsigned (&a)[4], unsigned b0,
-                                         unsigned b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-// 16 lanes x 32 columns from the m16n8 accumulator layout: register 2r holds
-// (lane t/4, column 4r + t%4), register 2r + 1 (lane t/4 + 8, same column)
-__device__ __forceinline__ void lgp_tmem_st16x128_x8(unsigned taddr, const unsigned (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.16x128b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-      "%15,%16};" ::"r"(taddr),
-      LGP_W8(v, 0), LGP_W8(v, 8)
-      : "memory");
+__device__ __forceinline__ void lgp_tmem_ld8(unsigned taddr, unsigned* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : LGP_R8(v, 0)
+               : "r"(taddr));
 }
 
 // FP16 hi/lo split of two FP32 values, packed {lo half = x0, hi half = x1}:
@@ -511,8 +351,8 @@ extern "C" __global__ void lgp_tc_prep(LgpPrepArgs p, int tile_rows, int is_col)
     h[3 * LGP_D + 1] = is_col ? (unsigned short)(one | sign) : nl;
     h[3 * LGP_D + 2] = is_col ? (unsigned short)(nh ^ sign) : one;
     h[3 * LGP_D + 3] = is_col ? (unsigned short)(nl ^ sign) : one;
-    // FP32 features for the chunks whose distances run on the FMA pipe:
-    // -r^2 = (-|c_i|^2) + (-|c_j|^2) + sum_d c_i[d] (2 c_j[d])
+    // FP32 point features [FW]: (c or 2c, -|c|^2, 0 ..), then from P0 the
+    // Periodic (cos, sin) blocks (read by the epilogues of Periodic trees)
     if (p.f32 != nullptr) {
       float* f = p.f32 + i * LGP_TC_FW;
 #pragma unroll
@@ -543,29 +383,10 @@ extern "C" __global__ void lgp_tc_prep(LgpPrepArgs p, int tile_rows, int is_col)
 }
 
 // ------------------------------------------------------------------ K1-TC
-// A CTA pair (cluster of 2 on one TPC) owns 256 rows: rank r holds rows
-// 128r..128r+127 of the pair's block in its SMEM / TMEM, stages its half of
-// every chunk's B operands, and runs its own epilogue; the leader (rank 0)
-// issues every tcgen05.mma of the pair (cta_group::2, M = 256), halving the
-// MMA instructions per row and the bulk-copy bytes per SM.
-#if LGP_TC_PAIR
-extern "C" __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
-#else
-extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
-#endif
-    lgp_matvec_tc(const LgpTcArgs a) {
-  if (a.done != nullptr && *a.done) return;  // same flag in both CTAs of a pair
-#if LGP_TC_PAIR
-  const unsigned rank = lgp_cluster_rank();
-  const int pair = blockIdx.x >> 1;
-  const int n_rbp = a.n_rb >> 1;
-  const int rb = 2 * (pair % n_rbp) + (int)rank;
-  const int rest = pair / n_rbp;
-#else
-  const unsigned rank = 0;
+extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const LgpTcArgs a) {
+  if (a.done != nullptr && *a.done) return;
   const int rb = blockIdx.x % a.n_rb;
   const int rest = blockIdx.x / a.n_rb;
-#endif
   const int seg = rest % a.n_seg;
   const int pass = rest / a.n_seg;
   const int tile0 = seg * a.tiles_per_seg;
@@ -588,35 +409,30 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (tid == 0) {
     lgp_mbar_init(BAR(B_AFULL), 1);
-    lgp_mbar_init(BAR(B_PAFULL), 1);
     for (int s = 0; s < LGP_TC_STAGES; ++s) {
       lgp_mbar_init(BAR(B_SFULL(s)), 1);
       lgp_mbar_init(BAR(B_SEMPTY(s)), 1);
-      lgp_mbar_init(BAR(B_PSFULL(s)), 1);
     }
     for (int q = 0; q < LGP_TC_NSB; ++q) {
       lgp_mbar_init(BAR(B_S1FULL(q)), 1);
-      lgp_mbar_init(BAR(B_PFULL(q)), TC_NEPI);
+      lgp_mbar_init(BAR(B_PFULL(q)), 4);
       lgp_mbar_init(BAR(B_PEMPTY(q)), 1);
     }
     for (int w = 0; w < 2; ++w)
       for (int b = 0; b < 2; ++b) {
         lgp_mbar_init(BAR(B_D2FULL(w, b)), 1);
-        lgp_mbar_init(BAR(B_D2EMPTY(w, b)), TC_NEPI);
+        lgp_mbar_init(BAR(B_D2EMPTY(w, b)), 4);
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::" TC_CG ".sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      lgp_saddr(tslot))
                  : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::" TC_CG ".sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   lgp_tc_fence_before();
   __syncthreads();
-#if LGP_TC_PAIR
-  lgp_cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
-#endif
   lgp_tc_fence_after();
   const unsigned tmem = *tslot;
   // TMEM columns: S buffer q: 64 FP32 columns of S', then P packed FP16 (hi in
@@ -625,11 +441,11 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
 #define T_D2(w, b) \
   (tmem + 64u * LGP_TC_NSB + (unsigned)TC_N2 * (2u * (unsigned)(w) + (unsigned)(b)))
 
-  // instruction descriptors: FP32 accumulate, FP16 A and B, K-major, M = TC_M.
+  // instruction descriptors: FP32 accumulate, FP16 A and B, K-major, M = 128.
   // Shared-memory descriptors are precomputed: the start-address field is
   // linear (a K step of 256 B adds 16, a stage adds STAGE_BYTES/16).
-  const unsigned idesc1 = (1u << 4) | ((unsigned)(TC_CH >> 3) << 17) | ((unsigned)(TC_M >> 4) << 24);
-  const unsigned idesc2 = (1u << 4) | ((unsigned)(TC_N2 >> 3) << 17) | ((unsigned)(TC_M >> 4) << 24);
+  const unsigned idesc1 = (1u << 4) | ((unsigned)(TC_CH >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
+  const unsigned idesc2 = (1u << 4) | ((unsigned)(TC_N2 >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
   const unsigned long long dk = lgp_sdesc(0u, LGP_TC_KD * 16);
   const unsigned long long dv = lgp_sdesc(0u, 1024u);
   const unsigned stg0 = lgp_saddr(stg) >> 4;
@@ -640,54 +456,36 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
       lgp_mbar_expect_tx(BAR(B_AFULL), TC_A1_BYTES);
       lgp_bulk_g2s(lgp_saddr(a1s), a.a1 + (size_t)rb * (TC_A1_BYTES / 4), TC_A1_BYTES, BAR(B_AFULL));
       const unsigned char* vbase = reinterpret_cast<const unsigned char*>(a.v);
-      TR_DECL
       for (int c = 0; c < nch; ++c) {
         const int s = c % LGP_TC_STAGES;
         if (c >= LGP_TC_STAGES) lgp_mbar_wait(BAR(B_SEMPTY(s)), ((c / LGP_TC_STAGES) - 1) & 1);
-        TR_MARK(0)
         const unsigned dst = lgp_saddr(stg + (size_t)s * TC_STAGE_BYTES);
-        lgp_mbar_expect_tx(BAR(B_SFULL(s)),
-                           TC_B1H_BYTES + TC_VH_BYTES + (TC_C32(c) ? TC_C32_BYTES : 0));
-        lgp_bulk_g2s(dst,
-                     reinterpret_cast<const unsigned char*>(a.b1) +
-                         (size_t)(tile0 + c) * TC_B1_BYTES + rank * TC_B1H_BYTES,
-                     TC_B1H_BYTES, BAR(B_SFULL(s)));
-        lgp_bulk_g2s(dst + TC_B1H_BYTES,
-                     vbase + ((size_t)pass * a.n_tiles + tile0 + c) * TC_V_BYTES +
-                         rank * TC_VH_BYTES,
-                     TC_VH_BYTES, BAR(B_SFULL(s)));
-        if (TC_C32(c))
-          lgp_bulk_g2s(dst + TC_B1H_BYTES + TC_VH_BYTES,
-                       reinterpret_cast<const unsigned char*>(a.c32) +
-                           (size_t)(tile0 + c) * TC_C32_BYTES,
-                       TC_C32_BYTES, BAR(B_SFULL(s)));
-        TR_MARK(1)
+        lgp_mbar_expect_tx(BAR(B_SFULL(s)), TC_STAGE_BYTES);
+        lgp_bulk_g2s(dst, reinterpret_cast<const unsigned char*>(a.b1) + (size_t)(tile0 + c) * TC_B1_BYTES,
+                     TC_B1_BYTES, BAR(B_SFULL(s)));
+        lgp_bulk_g2s(dst + TC_B1_BYTES, vbase + ((size_t)pass * a.n_tiles + tile0 + c) * TC_V_BYTES,
+                     TC_V_BYTES, BAR(B_SFULL(s)));
+#if LGP_TC_PF
+        lgp_bulk_g2s(dst + TC_B1_BYTES + TC_V_BYTES,
+                     reinterpret_cast<const unsigned char*>(a.c32) + (size_t)(tile0 + c) * TC_C32_BYTES,
+                     TC_C32_BYTES, BAR(B_SFULL(s)));
+#endif
       }
-      TR_FLUSH(0, 1)
     }
     __syncwarp();
-  } else if (warp == 11 && rank == 0) {
-    if (lane == 0 && LGP_TC_HMMA != 0xFF) {
-      // -------------------------------------- distance-GEMM issuer (leader)
-      // every chunk in order, once it is staged (in both CTAs of a pair) and
-      // its S buffer's previous contraction has completed (PEMPTY)
+  } else if (warp == 11) {
+    if (lane == 0) {
+      // --------------------------------------------- distance-GEMM issuer
+      // every chunk in order, once it is staged and its S buffer's previous
+      // contraction has completed (PEMPTY)
       const unsigned long long a_d = dk + (lgp_saddr(a1s) >> 4);
       lgp_mbar_wait(BAR(B_AFULL), 0);
-#if LGP_TC_PAIR
-      lgp_mbar_wait_cl(BAR(B_PAFULL), 0);
-#endif
-      TR_DECL
       for (int c = 0; c < nch; ++c) {
-        if (TC_SIMT(c) || TC_HMMA_CHUNK(c)) continue;  // distances from the FMA pipe / mma.sync
         const int w = c & 1, k = c >> 1;
         const int q = w + 2 * (k % TC_NSBW);
         const int s = c % LGP_TC_STAGES;
         lgp_mbar_wait(BAR(B_SFULL(s)), (c / LGP_TC_STAGES) & 1);
-#if LGP_TC_PAIR
-        lgp_mbar_wait_cl(BAR(B_PSFULL(s)), (c / LGP_TC_STAGES) & 1);
-#endif
         if (k >= TC_NSBW) lgp_mbar_wait(BAR(B_PEMPTY(q)), ((k / TC_NSBW) - 1) & 1);
-        TR_MARK(3)
         lgp_tc_fence_after();
         const unsigned long long b_d = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
         const unsigned d = T_SB(q);
@@ -695,66 +493,40 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int kk = 0; kk < LGP_TC_KD / 16; ++kk)
           lgp_mma_f16_ss(d, a_d + 16u * kk, b_d + 16u * kk, idesc1, kk > 0);
         lgp_mma_commit(BAR(B_S1FULL(q)));
-        TR_MARK(4)
-      }
-      TR_FLUSH(3, 4)
-    }
-    __syncwarp();
-  } else if ((warp == 1 || warp >= 10) && rank == 1) {
-#if LGP_TC_PAIR
-    if (warp == 1 && lane == 0) {
-      // ------------------------------------------------ peer relay
-      // the leader issues MMAs that read this CTA's staged operands: forward
-      // this CTA's bulk-copy completions to the leader's P* barriers
-      lgp_mbar_wait(BAR(B_AFULL), 0);
-      lgp_mbar_arrive_cluster(lgp_mapa(BAR(B_PAFULL), 0));
-      for (int c = 0; c < nch; ++c) {
-        const int s = c % LGP_TC_STAGES;
-        lgp_mbar_wait(BAR(B_SFULL(s)), (c / LGP_TC_STAGES) & 1);
-        lgp_mbar_arrive_cluster(lgp_mapa(BAR(B_PSFULL(s)), 0));
       }
     }
     __syncwarp();
-#endif
   } else if (warp == 1 || warp == 10) {
     if (lane == 0) {
-      // -------------------------------------- contraction issuers (leader)
-      // An MMA-issuing thread sustains one tcgen05.mma per ~60-90 cycles, so
+      // -------------------------------------------- contraction issuers
       // each epilogue warpgroup w has its own contraction issuer (warp 1 ->
-      // w 0, warp 10 -> w 1) that owns its D2 accumulators.
+      // w 0, warp 10 -> w 1) that owns its D2 accumulators
       const int w = warp == 1 ? 0 : 1;
       const int nloc = (nch - w + 1) >> 1;
-      TR_DECL
       for (int k = 0; k < nloc; ++k) {
         const int c = 2 * k + w;
         const int q = w + 2 * (k % TC_NSBW);
         const int gi = k / LGP_TC_G, b = gi & 1;
         const bool first = (k % LGP_TC_G) == 0;
         const bool last = ((k % LGP_TC_G) == LGP_TC_G - 1) || (k == nloc - 1);
-        TR_MARK(5)
-        lgp_mbar_wait_ld(BAR(B_PFULL(q)), (k / TC_NSBW) & 1);
-        if (first && gi >= 2) lgp_mbar_wait_ld(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
-        TR_MARK(6)
+        lgp_mbar_wait(BAR(B_PFULL(q)), (k / TC_NSBW) & 1);
+        if (first && gi >= 2) lgp_mbar_wait(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
         lgp_tc_fence_after();
         const int s = c % LGP_TC_STAGES;
-        // B = [V_hi ; V_lo] (on a pair: rank 0 stages the hi rows, rank 1 the lo rows)
-        const unsigned long long v_d =
-            dv + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4) + (TC_B1H_BYTES >> 4);
+        // B = [V_hi ; V_lo]
+        const unsigned long long v_d = dv + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4) + (TC_B1_BYTES >> 4);
         const unsigned d = T_D2(w, b);
         const unsigned p = T_SB(q);
 #pragma unroll
         for (int kk = 0; kk < TC_CH / 16; ++kk) {
           const unsigned o = 16u * kk;
-          if ((LGP_TC_ABLATE & 1) && kk > 0) break;
           lgp_mma_f16_ts(d, p + 8u * kk, v_d + o, idesc2, (first && kk == 0) ? 0u : 1u);
           lgp_mma_f16_ts(d, p + 32u + 8u * kk, v_d + o, idesc2, 1u);
         }
         lgp_mma_commit(BAR(B_SEMPTY(s)));
-        lgp_mma_commit_local(BAR(B_PEMPTY(q)));
+        lgp_mma_commit(BAR(B_PEMPTY(q)));
         if (last) lgp_mma_commit(BAR(B_D2FULL(w, b)));
-        TR_MARK(7)
       }
-      TR_FLUSH(5, 7)
     }
     __syncwarp();
   } else {
@@ -767,26 +539,6 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
     double acc[LGP_TC_N];
 #pragma unroll
     for (int i = 0; i < LGP_TC_N; ++i) acc[i] = 0.0;
-#if LGP_TC_HMMA
-    // A fragments of this warp's 32 rows (2 m16 tiles x KD/16 k-steps), once
-    lgp_mbar_wait(BAR(B_AFULL), 0);
-    unsigned af[2][LGP_TC_KD / 16][4];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int ks = 0; ks < LGP_TC_KD / 16; ++ks) {
-        const int mi = lane >> 3;
-        const int r = 32 * q4 + 16 * mt + (mi & 1) * 8 + (lane & 7);
-        const int kc = 2 * ks + (mi >> 1);
-        lgp_ldsm_x4(lgp_saddr(a1s) + (unsigned)((r >> 3) * (LGP_TC_KD * 16) + kc * 128 + (r & 7) * 16),
-                    af[mt][ks]);
-      }
-#endif
-#if LGP_TC_SIMT_MASK
-    float rf32[LGP_D + 1];  // this thread's row: (c_i, -|c_i|^2)
-#pragma unroll
-    for (int d = 0; d <= LGP_D; ++d) rf32[d] = a.r32[((size_t)rb * 128 + row) * LGP_TC_FW + d];
-#endif
 #if LGP_TC_PF
     float frp[LGP_TC_PF];  // this thread's row: Periodic (cos, sin) features
 #pragma unroll
@@ -801,129 +553,46 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
       // columns 0..N-1: P.V_hi, N..2N-1: P.V_lo
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        unsigned v[16];
-        lgp_tmem_ld16(T_D2(w, b) + lanes + 16u * h, v);
+#if LGP_TC_N == 8
+        unsigned v[8];
+        lgp_tmem_ld8(T_D2(w, b) + lanes + 8u * h, v);
         lgp_tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] += (double)__uint_as_float(v[i]);
+        for (int i = 0; i < 8; ++i) acc[i] += (double)__uint_as_float(v[i]);
+#else
+#pragma unroll
+        for (int b16 = 0; b16 < LGP_TC_N / 16; ++b16) {
+          unsigned v[16];
+          lgp_tmem_ld16(T_D2(w, b) + lanes + (unsigned)(LGP_TC_N * h + 16 * b16), v);
+          lgp_tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[16 * b16 + i] += (double)__uint_as_float(v[i]);
+        }
+#endif
       }
       lgp_tc_fence_before();
       __syncwarp();
-      if (lane == 0) lgp_arrive_leader(BAR(B_D2EMPTY(w, b)));
+      if (lane == 0) lgp_mbar_arrive(BAR(B_D2EMPTY(w, b)));
     };
 
-    TR_DECL
-    // S1FULL(q) completes once per distance-GEMM use of buffer q; with
-    // FMA-pipe chunks interleaved, its phase is tracked per buffer slot
-    unsigned s1par = 0;
     for (int k = 0; k < nloc; ++k) {
       const int q = w + 2 * (k % TC_NSBW);
       const unsigned sb = T_SB(q) + lanes;
-#if LGP_TC_HMMA
-      if (TC_HMMA_CHUNK(2 * k + w)) {
-        // -r^2 of this warp's 32 rows x 64 columns by mma.sync (FP32 in
-        // registers), straight into the tree and the FP16 hi/lo split; P goes to
-        // TMEM in the accumulator layout (tcgen05.st 16x128b), no S round trip
-        const int c = 2 * k + w;
-        const int st = c % LGP_TC_STAGES;
-        lgp_mbar_wait(BAR(B_SFULL(st)), (c / LGP_TC_STAGES) & 1);  // column features staged
-        if (k >= TC_NSBW) lgp_mbar_wait(BAR(B_PEMPTY(q)), ((k / TC_NSBW) - 1) & 1);  // P buffer free
-        if (lane == 0) { TR_MARK(9) }
-        lgp_tc_fence_after();
-        const unsigned b1s = lgp_saddr(stg + (size_t)st * TC_STAGE_BYTES);
-        float cf[2][8][4];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) cf[mt][nt][e] = 0.f;
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-          for (int ks = 0; ks < LGP_TC_KD / 16; ++ks) {
-            const int nrow = 8 * nt + (lane & 7);
-            const int kc = 2 * ks + ((lane >> 3) & 1);
-            unsigned b0, b1;
-            lgp_ldsm_x2(b1s + (unsigned)((nrow >> 3) * (LGP_TC_KD * 16) + kc * 128 + (nrow & 7) * 16),
-                        b0, b1);
-            lgp_hmma(cf[0][nt], af[0][ks], b0, b1);
-            lgp_hmma(cf[1][nt], af[1][ks], b0, b1);
-          }
-        unsigned hw[2][16], lw[2][16];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 8; ++nt) {
-            const int px = nt < (LGP_TC_POLY + 1) / 2 ? 1 : 0;
-            const int px1 = nt < LGP_TC_POLY / 2 ? 1 : 0;
-            float kv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              kv[e] = lgp_tc_k(LGP_TC_CLAMP(cf[mt][nt][e]), a, (e & 1) ? px1 : px);
-            lgp_split_f16x2(kv[0], kv[1], hw[mt][2 * nt], lw[mt][2 * nt]);
-            lgp_split_f16x2(kv[2], kv[3], hw[mt][2 * nt + 1], lw[mt][2 * nt + 1]);
-          }
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          lgp_tmem_st16x128_x8(sb + ((16u * mt) << 16), hw[mt]);        // hi pairs: columns 0..31
-          lgp_tmem_st16x128_x8(sb + ((16u * mt) << 16) + 32u, lw[mt]);  // lo pairs: columns 32..63
-        }
-      } else
-#endif
-      {
       unsigned s[64];
-      if (lane == 0) { TR_MARK(8) }
-#if LGP_TC_SIMT_MASK
-      const int c = 2 * k + w;
-      if (TC_SIMT(c)) {
-        // -r^2 on the FMA pipe from the staged FP32 column features (every
-        // lane reads the same column: broadcast); the S buffer is free once
-        // the contraction that last read it has completed
-        const int st = c % LGP_TC_STAGES;
-        lgp_mbar_wait(BAR(B_SFULL(st)), (c / LGP_TC_STAGES) & 1);
-        if (k >= TC_NSBW) lgp_mbar_wait(BAR(B_PEMPTY(q)), ((k / TC_NSBW) - 1) & 1);
-        if (lane == 0) { TR_MARK(9) }
-        lgp_tc_fence_after();
-        const float4* cf = reinterpret_cast<const float4*>(
-            stg + (size_t)st * TC_STAGE_BYTES + TC_B1H_BYTES + TC_VH_BYTES);
-#pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          float cj[LGP_TC_FW];
-#pragma unroll
-          for (int f4 = 0; f4 < LGP_TC_FW / 4; ++f4) {
-            const float4 v4 = cf[j * (LGP_TC_FW / 4) + f4];
-            cj[4 * f4 + 0] = v4.x;
-            cj[4 * f4 + 1] = v4.y;
-            cj[4 * f4 + 2] = v4.z;
-            cj[4 * f4 + 3] = v4.w;
-          }
-          float acc = rf32[LGP_D] + cj[LGP_D];
-#pragma unroll
-          for (int d = 0; d < LGP_D; ++d) acc = fmaf(rf32[d], cj[d], acc);
-          s[j] = __float_as_uint(acc);
-        }
-      } else
-#endif
-      {
-        const int slot = k % TC_NSBW;
-        lgp_mbar_wait(BAR(B_S1FULL(q)), (s1par >> slot) & 1u);
-        s1par ^= 1u << slot;
-        if (lane == 0) { TR_MARK(9) }
-        lgp_tc_fence_after();
-        // all 64 columns in one round trip; P overwrites S' in the same
-        // registers: s[2m] = FP16x2 hi of entries (2m, 2m+1), s[2m+1] = lo
-        lgp_tmem_ld32p(sb, s);
-        lgp_tmem_ld32p(sb + 32u, s + 32);
-        lgp_tmem_wait_ld();
-      }
+      lgp_mbar_wait(BAR(B_S1FULL(q)), (k / TC_NSBW) & 1);
+      lgp_tc_fence_after();
+      // all 64 columns in one round trip; P overwrites S' in the same
+      // registers: s[2m] = FP16x2 hi of entries (2m, 2m+1), s[2m+1] = lo
+      lgp_tmem_ld32p(sb, s);
+      lgp_tmem_ld32p(sb + 32u, s + 32);
+      lgp_tmem_wait_ld();
 #if LGP_TC_PF
       // column Periodic features of this chunk, staged with its B tile (the
       // stage is released only after this chunk's contraction)
       const int cpf = 2 * k + w;
       lgp_mbar_wait(BAR(B_SFULL(cpf % LGP_TC_STAGES)), (cpf / LGP_TC_STAGES) & 1);
       const float* cfp = reinterpret_cast<const float*>(stg + (size_t)(cpf % LGP_TC_STAGES) * TC_STAGE_BYTES +
-                                                        TC_B1H_BYTES + TC_VH_BYTES) + LGP_TC_P0;
+                                                        TC_B1_BYTES + TC_V_BYTES) + LGP_TC_P0;
 #define TC_KJ(x, pxv, j) lgp_tc_kf((x), a, (pxv), frp, cfp + (j) * LGP_TC_FW)
 #else
 #define TC_KJ(x, pxv, j) lgp_tc_k((x), a, (pxv))
@@ -937,30 +606,26 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
         lgp_split_f16x2(k0, k1, s[2 * m], s[2 * m + 1]);
       }
 #undef TC_KJ
-      lgp_tmem_st32s2(sb, s);        // hi pairs -> columns 0..31
+      lgp_tmem_st32s2(sb, s);            // hi pairs -> columns 0..31
       lgp_tmem_st32s2(sb + 32u, s + 1);  // lo pairs -> columns 32..63
-      }
       lgp_tmem_wait_st();
       lgp_tc_fence_before();
       __syncwarp();
-      if (lane == 0) lgp_arrive_leader(BAR(B_PFULL(q)));
-      if (lane == 0) { TR_MARK(10) }
+      if (lane == 0) lgp_mbar_arrive(BAR(B_PFULL(q)));
       // drain a finished accumulation group DLAG chunks into the next one, so
       // its last contraction has long completed (DLAG <= G keeps at most two
       // groups, i.e. both D2 buffers, outstanding)
       if (k >= LGP_TC_DLAG && ((k - LGP_TC_DLAG) % LGP_TC_G) == LGP_TC_G - 1)
         drain((k - LGP_TC_DLAG) / LGP_TC_G);
-      if (lane == 0) { TR_MARK(11) }
     }
     for (int gi = nloc >= LGP_TC_DLAG ? (nloc - LGP_TC_DLAG) / LGP_TC_G : 0;
          gi < (nloc + LGP_TC_G - 1) / LGP_TC_G; ++gi)
       drain(gi);
-    if (lane == 0) { TR_FLUSH(8, 11) }
 
     // combine the two warpgroups' FP64 sums in a fixed order, undo the V scaling
     if (w == 1) {
 #pragma unroll
-      for (int i = 0; i < LGP_TC_N; ++i) comb[row * LGP_TC_N + i] = acc[i];
+      for (int i = 0; i < LGP_TC_N; ++i) comb[i * 128 + row] = acc[i];
     }
     asm volatile("bar.sync 1, 256;" ::: "memory");
     if (w == 0) {
@@ -970,20 +635,17 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1)
       const float* sc = a.vscale + (size_t)pass * LGP_TC_N;
 #pragma unroll
       for (int i = 0; i < LGP_TC_N; i += 2) {
-        const double x0 = (acc[i] + comb[row * LGP_TC_N + i]) * (double)sc[i];
-        const double x1 = (acc[i + 1] + comb[row * LGP_TC_N + i + 1]) * (double)sc[i + 1];
+        const double x0 = (acc[i] + comb[i * 128 + row]) * (double)sc[i];
+        const double x1 = (acc[i + 1] + comb[(i + 1) * 128 + row]) * (double)sc[i + 1];
         reinterpret_cast<double2*>(out)[i / 2] = make_double2(x0, x1);
       }
     }
   }
   lgp_tc_fence_before();
   __syncthreads();
-#if LGP_TC_PAIR
-  lgp_cluster_sync();  // no MMA of the pair is pending on either TMEM
-#endif
   if (warp == 0) {
     lgp_tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::" TC_CG ".sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 #undef BAR
 #undef T_SB

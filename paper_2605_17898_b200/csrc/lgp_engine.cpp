@@ -266,7 +266,7 @@ void MatvecOp::prepare() {
   if (t == 1 && rows == cols && (!ctx->sharded() || rank_split) && row0 == 0 && n_rows == rows->n &&
       !(flags & (LGP_NO_SYM | LGP_FORCE_SIMT | LGP_DIST_DIRECT)) && !std::getenv("LGP_NO_TCSYM")) {
     Plan p = make_tc_plan(k->tree, rows->d, 16, flags);
-    if (p.tc && !p.tc_pair && p.ts_rmax >= 1) {
+    if (p.tc && p.ts_rmax >= 1) {
       plan = p;
       tcsym = true;
     }
@@ -287,7 +287,6 @@ void MatvecOp::prepare() {
   const Tuning& tu = plan.tune;
   const int rows_per_cta = plan.tc ? 128 : tu.threads * tu.r;
   n_rb = (int)ceil_div<int64_t>(std::max<int64_t>(n_rows, 1), rows_per_cta);
-  if (plan.tc && plan.tc_pair) n_rb += n_rb & 1;  // CTA pairs: 256-row blocks
   n_rows_pad = n_rb * rows_per_cta;
   const int cc = plan.tc ? 64 : tu.cc;
   n_tiles = (int)ceil_div<int64_t>(std::max<int64_t>(cols->n, 1), cc);
@@ -318,7 +317,7 @@ void MatvecOp::prepare() {
     // operands pre-tiled in the UMMA canonical layout, FP16 hi/lo split
     fr = (float*)ctx->scratch_get(tag + ".a1", (size_t)n_rows_pad * plan.tc_kd * 2);
     fc = (float*)ctx->scratch_get(tag + ".b1", (size_t)n_cols_pad * plan.tc_kd * 2);
-    if (plan.tc_simt || plan.tc_pf > 0) {
+    if (plan.tc_pf > 0) {
       r32 = (float*)ctx->scratch_get(tag + ".r32", (size_t)n_rows_pad * plan.tc_fw * 4);
       c32 = (float*)ctx->scratch_get(tag + ".c32", (size_t)n_cols_pad * plan.tc_fw * 4);
     }
@@ -513,30 +512,9 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     a.n_tiles = n_tiles;
     const int64_t grid = (int64_t)n_rb * n_seg * n_pass;
     if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
-    unsigned long long* trace = nullptr;
-    if (std::getenv("LGP_TC_TRACE")) {
-      trace = (unsigned long long*)ctx->scratch_get("tc.trace", 16 * 8);
-      LGP_CUDA_CHECK(cudaMemsetAsync(trace, 0, 16 * 8, ctx->stream));
-    }
-    a.trace = trace;
     prof_begin();
-    if (plan.tc_v5)
-      launch(ctx, mod->tc4, (unsigned)grid, 1, 96 + 128 * plan.t4_nwg, plan.smem_tc4, &a);
-    else
-      launch(ctx, mod->matvec, (unsigned)grid, 1, plan.tune.threads, plan.smem_bytes, &a);
+    launch(ctx, mod->matvec, (unsigned)grid, 1, plan.tune.threads, plan.smem_bytes, &a);
     prof_end();
-    if (trace) {
-      unsigned long long h[16];
-      LGP_CUDA_CHECK(cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
-      LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-      const double ctas = (double)grid;
-      fprintf(stderr,
-              "[tc trace, cycles per CTA] producer: wait %.0f issue %.0f | gemm1: wait %.0f issue %.0f "
-              "| gemm2 issuers (sum of 2): wait %.0f issue %.0f | "
-              "wg(per warp): wait_d1 %.0f epi %.0f drain %.0f\n",
-              h[0] / ctas, h[1] / ctas, h[3] / ctas, h[4] / ctas, h[6] / ctas, h[7] / ctas,
-              h[9] / ctas / 8, h[10] / ctas / 8, h[11] / ctas / 8);
-    }
     vec::epilogue(ctx, partial, n_seg, n_pass, n_rows_pad, tb, n_rows, t, plan.root_scale, noise,
                   noise_v, out_dev, done);
     return;
@@ -684,11 +662,8 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   // SIMT), CG counts its iterations. Multi-RHS CG (predictive variance, t = T
   // test points): the tensor-core K1 - its rounding-level asymmetry costs
   // iterations (~1.3x) but each costs 4.5x less than the SIMT kernel's t/16
-  // passes (cfg4, T = 200: 47 vs 210 ms); LGP_CG_TC=0/1 overrides.
-  if (const char* e = std::getenv("LGP_CG_TC"))
-    op.allow_tc = atoi(e) != 0;
-  else
-    op.allow_tc = t >= 8;
+  // passes (cfg4, T = 200: 47 vs 210 ms).
+  op.allow_tc = t >= 8;
   if (ctx->sharded() && t == 1 && !std::getenv("LGP_NO_RANK_SPLIT")) {
     // try the rank-split symmetric schedule: all rows, a share of the pairs
     op.rank_split = true;

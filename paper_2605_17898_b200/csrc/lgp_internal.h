@@ -99,17 +99,12 @@ struct Plan {
   bool tc = false;
   int tc_kd = 0;            // K of the distance GEMM in FP16 halves (3D + 4, multiple of 16)
   int tc_n = 16;            // RHS per pass (GEMM2 N)
-  bool tc_pair = false;     // K1-TC on CTA pairs (cta_group::2, 256-row blocks)
   int tc_fw = 0;            // FP32 features per point for FMA-pipe distance chunks
   int tc_pf = 0;            // of which Periodic (cos, sin) features, from offset P0
-  bool tc_simt = false;     // some K1-TC chunks compute distances on the FMA pipe
   size_t smem_tcsym = 0;    // dynamic shared memory of lgp_matvec_tcsym (at R = kTsRMax)
   size_t smem_tcsym_fixed = 0;  // ... without the [2R][64] column accumulators
   int ts_rmax = 0;              // largest super-tile R that fits the shared memory
   int ts_nwg = 3;           // lgp_matvec_tcsym epilogue warpgroups
-  bool tc_v5 = false;       // use lgp_matvec_tc4 (mma.sync distance tiles) for t > 1
-  int t4_nwg = 4;
-  size_t smem_tc4 = 0;
   LgpTcArgs tca{};          // kc[] filled
 };
 
@@ -134,7 +129,6 @@ struct Module {
   CUfunction prep = nullptr, matvec = nullptr, gram = nullptr, diag = nullptr;
   CUfunction matvec_sym = nullptr;  // symmetric-operator K1 (SIMT modules)
   CUfunction tcsym = nullptr;       // symmetric tensor-core K1, t = 1 (TC modules)
-  CUfunction tc4 = nullptr;         // K1-TC with mma.sync distance tiles (TC modules)
   bool tc = false;  // module holds lgp_tc_prep / lgp_matvec_tc in prep / matvec
   int blocks_per_sm = 1;
   int regs = 0;

@@ -175,13 +175,8 @@ Module* get_module(Context* ctx, const Plan& plan) {
   if (plan.tc) {
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->prep, m->mod, "lgp_tc_prep"));
     LGP_CU_CHECK(drv::ModuleGetFunction(&m->matvec, m->mod, "lgp_matvec_tc"));
-    if (!plan.tc_pair) {
+    {
       LGP_CU_CHECK(drv::ModuleGetFunction(&m->tcsym, m->mod, "lgp_matvec_tcsym"));
-      if (plan.tc_v5) {
-        LGP_CU_CHECK(drv::ModuleGetFunction(&m->tc4, m->mod, "lgp_matvec_tc4"));
-        LGP_CU_CHECK(drv::FuncSetAttribute(m->tc4, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                                           (int)plan.smem_tc4));
-      }
       if (plan.smem_tcsym > 0)
         LGP_CU_CHECK(drv::FuncSetAttribute(m->tcsym, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                                            (int)plan.smem_tcsym));

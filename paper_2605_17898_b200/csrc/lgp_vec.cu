@@ -126,7 +126,7 @@ __global__ void k_dot_final(const double* part, int nblk, int t, double* out, co
 }
 
 __global__ void k_pack(const double* __restrict__ V, long long n, int t, long long n_pad, int tb,
-                       int n_pass, double* __restrict__ out, const int* done, int drop_bits) {
+                       int n_pass, double* __restrict__ out, const int* done) {
   if (is_done(done)) return;
   const long long total = (long long)n_pass * n_pad * tb;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -136,9 +136,6 @@ __global__ void k_pack(const double* __restrict__ V, long long n, int t, long lo
     const int p = (int)(e / ((long long)tb * n_pad));
     const int c = p * tb + cc;
     double v = (j < n && c < t) ? V[j * t + c] : 0.0;
-    // experiment (LGP_EMU_VBITS): keep only 52 - drop_bits mantissa bits of V,
-    // emulating the RHS rounding of a tensor-core contraction
-    if (drop_bits) v = __longlong_as_double(__double_as_longlong(v) & ~((1ll << drop_bits) - 1));
     out[e] = v;
   }
 }
@@ -966,9 +963,8 @@ int reduce_blocks(int64_t n, int t) {
 
 void pack_rhs(Context* c, const double* V, int64_t n, int t, int64_t n_pad, int tb, int n_pass,
               double* out, const int* done) {
-  static const int drop = std::getenv("LGP_EMU_VBITS") ? 52 - atoi(std::getenv("LGP_EMU_VBITS")) : 0;
   k_pack<<<grid_for((long long)n_pass * n_pad * tb), 256, 0, c->stream>>>(V, n, t, n_pad, tb,
-                                                                         n_pass, out, done, drop);
+                                                                         n_pass, out, done);
   LGP_LAUNCH_CHECK(c);
 }
 
@@ -1141,7 +1137,7 @@ void lz_update1(Context* c, double* w, const double* q, const double* qprev, int
 void lz_multidot(Context* c, const double* basis, int64_t stride, int nb, const double* w,
                  int64_t n, int t, double* part, const int* done) {
   const int nblk = reduce_blocks(n, t);
-  if (2 * t <= 256 && !std::getenv("LGP_LZ_MULTIDOT1")) {
+  if (2 * t <= 256) {
     const int kb = 256 / t;
     k_lz_multidot2<<<dim3(nblk, (nb + kb - 1) / kb), kb * t, 0, c->stream>>>(
         basis, stride, nb, w, n, t, chunk_rows(n, nblk), part, done);

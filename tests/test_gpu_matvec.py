@@ -343,20 +343,34 @@ def test_results_in_pinned_buffers_survive(gpu_ctx):
     np.testing.assert_allclose(c, a_copy, rtol=0, atol=0)
 
 
-@pytest.mark.parametrize("env", [{"LGP_TC_PAIR": "1"}, {"LGP_TC_SIMT_MASK": "0x48"},
-                                 {"LGP_TC_POLY": "0"}, {"LGP_TC_G": "2", "LGP_TC_DLAG": "1"},
-                                 {"LGP_TC_HMMA": "0x88"}, {"LGP_TC_V5": "1"},
-                                 {"LGP_TC_V5": "1", "LGP_T4_NWG": "3"}])
-def test_tensor_core_variants_parity(gpu_ctx, monkeypatch, env):
-    """The opt-in K1-TC variants (CTA pairs with cta_group::2, FMA-pipe or
-    mma.sync distance tiles, the mma.sync v5 kernel, MUFU-only exp2, other
-    drain schedules) meet the same bar."""
+@pytest.mark.parametrize("env", [{"LGP_TC_POLY": "0"}, {"LGP_TC_POLY": "4"},
+                                 {"LGP_TC_G": "2", "LGP_TC_DLAG": "1"}, {"LGP_TC_STAGES": "4"}])
+def test_tensor_core_tuning_parity(gpu_ctx, monkeypatch, env):
+    """K1-TC tuning knobs (exponentials on the FMA pipe per 16 entries, FP32
+    accumulation group / drain lag, TMA ring depth) meet the same bar."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     expr = "(+ (scale 2.0 (rbf 0.4)) (scale 0.5 (matern32 0.9)))"
     rng = np.random.default_rng(11)
     x = rng.random((3001, 6))
     V = rng.standard_normal((3001, 16))
+    got = _mv_flags(expr, x, V, 0.1, 0)
+    assert rel_l2(got, O.matvec(O.parse_tree(expr), x, 0.1, V)) <= TOL
+
+
+@pytest.mark.parametrize("t", [8, 9, 16, 17, 32, 33, 64, 100])
+@pytest.mark.parametrize("expr,d", [("(rbf 0.5)", 8), ("(matern32 0.5)", 8),
+                                    ("(+ (scale 1.0 (rbf 0.5)) (scale 1.0 (periodic 1.0 1.0)))", 2)])
+def test_tensor_core_rhs_widths(gpu_ctx, t, expr, d):
+    """K1-TC runs 8, 16 or 32 right-hand sides per pass (GEMM2 N = 16 / 32 /
+    64; t > 32 in passes of 32): every width, ragged t included, meets the
+    bar against the oracle, with Gaussian and +-1 columns."""
+    rng = np.random.default_rng(t)
+    n = 2500
+    x = rng.random((n, d))
+    V = rng.standard_normal((n, t))
+    V[:, ::3] = np.where(V[:, ::3] > 0, 1.0, -1.0)
+    assert "lgp_matvec_tc(" in G.kernels.program(G.parse_kernel(expr)).source(d, t)
     got = _mv_flags(expr, x, V, 0.1, 0)
     assert rel_l2(got, O.matvec(O.parse_tree(expr), x, 0.1, V)) <= TOL
 
