@@ -21,6 +21,7 @@ drop-in's scope and raise NotImplementedError.
 from __future__ import annotations
 
 import math
+import warnings
 import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -136,6 +137,14 @@ def gp_predict(state, x_star):
     _lib.check(lib.lgp_predict_quad(ctx.handle, op.prog.handle, op.points.handle, test.handle,
                                     state.noise, cfg.rel_tolerance, mi, _lib.dptr(quad),
                                     _lib.iptr(iters), _lib.dptr(res)))
+    cap = mi if mi > 0 else min(state.x_train.shape[0], 1000)
+    capped = int(np.count_nonzero(iters >= cap))
+    if capped:
+        # the reference reports a non-converged solve instead of raising
+        # (solvers.py:122-123) and gp_predict ignores it; say so
+        warnings.warn(f"gp_predict: the variance CG of {capped} of {t} test points stopped at the "
+                      f"{cap}-iteration budget (tolerance {cfg.rel_tolerance:g} not reached)",
+                      RuntimeWarning, stacklevel=2)
     var = prior - quad
     np.maximum(var, 0.0, out=var)
     return tracked(mean), tracked(var)
@@ -230,11 +239,18 @@ def optimize_hyperparams(objective, p0, config):
                     q = p.copy()
                     q[i] = p[i] + sgn * h
                     pts.append(q)
-            vals = iter([float(v) for v in batch(pts)])
+            # each point's value, or the exception its evaluation raised: an
+            # exception surfaces only when the replayed sequential order
+            # reaches that point (the reference stops at the first non-finite
+            # value and never evaluates the rest)
+            vals = iter(batch(pts, return_exceptions=True))
 
             def call(q, _vals=vals):
                 config.evaluations += 1
-                return next(_vals)
+                v = next(_vals)
+                if isinstance(v, BaseException):
+                    raise v
+                return float(v)
         centre = call(p)
         if not math.isfinite(centre):
             break
@@ -291,12 +307,24 @@ class _EvidenceObjective:
             ctx = self._ctx.ctx = _lib.Context(_lib.default_context().device)
         return self._eval(q, ctx)
 
-    def batch(self, qs):
+    def batch(self, qs, return_exceptions=False):
+        """Values of every q (concurrently); with return_exceptions an
+        evaluation that raises yields its exception in place of its value."""
+        def guard(fn):
+            def run(q):
+                try:
+                    return fn(q)
+                except Exception as exc:  # noqa: BLE001 (returned, re-raised by the caller)
+                    if not return_exceptions:
+                        raise
+                    return exc
+            return run
+
         if self.workers <= 1 or len(qs) <= 1:
-            return [self._eval(q) for q in qs]
+            return [guard(self._eval)(q) for q in qs]
         if self._pool is None:
             self._pool = ThreadPoolExecutor(max_workers=self.workers)
-        return list(self._pool.map(self._worker_eval, qs))
+        return list(self._pool.map(guard(self._worker_eval), qs))
 
 
 def exact_evidence_objective(x, y, kernel, cg_config=None, seed=0, workers=None):

@@ -227,3 +227,47 @@ def test_optimizer_matches_reference_bitwise():
 
     best, trace = G.optimize_hyperparams(bad, np.ones(2), G.OptimizerConfig(steps=10))
     assert len(trace) == 1 and np.array_equal(best, np.ones(2))
+
+
+def test_batched_optimizer_replays_exceptions_in_reference_order():
+    """A batched objective evaluates all 2P + 1 points of a step at once; an
+    evaluation that raises must surface only if the reference's sequential
+    call order reaches it: here the first up-step is NaN, so
+    the reference evaluates centre, up0, down0 and stops - the raising up1 is
+    never reached."""
+
+    class Obj:
+        def __init__(self):
+            self.seen = 0
+
+        def __call__(self, q):
+            raise AssertionError("the batch path must be used")
+
+        def batch(self, qs, return_exceptions=False):
+            self.seen += len(qs)
+            out = []
+            for i, q in enumerate(qs):
+                if i == 1:
+                    out.append(float("nan"))  # up0
+                elif i == 3:
+                    exc = ValueError("evaluation 3 fails")  # up1: never reached
+                    if not return_exceptions:
+                        raise exc
+                    out.append(exc)
+                else:
+                    out.append(-float(np.sum(q * q)))
+            return out
+
+    cfg = G.OptimizerConfig(steps=4, learning_rate=0.1)
+    obj = Obj()
+    best, trace = G.optimize_hyperparams(obj, np.array([0.2, -0.1]), cfg)
+    assert cfg.evaluations == 3 and len(trace) == 1 and obj.seen == 5
+    np.testing.assert_array_equal(best, [0.2, -0.1])
+
+    class Obj2(Obj):
+        def batch(self, qs, return_exceptions=False):
+            # the failing evaluation IS reached (it is the first up-step)
+            return [-1.0] + [ValueError("reached")] * (len(qs) - 1)
+
+    with pytest.raises(ValueError, match="reached"):
+        G.optimize_hyperparams(Obj2(), np.array([0.2, -0.1]), G.OptimizerConfig(steps=2))
