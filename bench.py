@@ -57,7 +57,7 @@ DTYPE_TC = ("f32 kernel entries from an FP16x2-split tcgen05 distance GEMM (FP32
 
 def tc_rhs_per_pass(t):
     """Right-hand sides per K1-TC pass (lgp_codegen.cpp make_tc_plan)."""
-    return 8 if t <= 8 else (16 if t <= 16 else 32)
+    return 8 if t <= 8 else (16 if t <= 16 else (32 if t <= 32 else 64))
 
 
 def flops_per_entry(kernel_expr, d, t):
@@ -432,11 +432,12 @@ def run_ours(args, rank, world):
     bf16 = float(pk.get("bf16_tflops", 1648.7))
     if tc:
         # K1-TC: per 128 x 64 chunk the distance GEMM (K = 3D+4 rounded to 16)
-        # and the contraction (K = 2 x 64, N = 2 x RHS per pass) on tcgen05
+        # and the contraction (K = 2 x 64, N = 2 x RHS; 64 RHS: 3 x K = 64, N = RHS) on tcgen05
         n_pass = -(-t // tc_rhs_per_pass(t))
         kh = -(-(3 * d + 4) // 16) * 16
         chunks = -(-rows_local // 128) * -(-n // 64) * n_pass
-        tflop = chunks * (2 * 128 * 64 * kh + 2 * 128 * (2 * tc_rhs_per_pass(t)) * 128) \
+        rhs = tc_rhs_per_pass(t)
+        tflop = chunks * (2 * 128 * 64 * kh + (3 * 2 * 128 * rhs * 64 if rhs == 64 else 2 * 128 * 2 * rhs * 128)) \
             / (k1_avg_ms * 1e-3) / 1e12
         roofline = {"bound": "sfu", "achieved": sfu_ach, "peak": sfu_peak, "unit": "T SFU op/s",
                     "frac": sfu_ach / sfu_peak, "traffic": traffic,

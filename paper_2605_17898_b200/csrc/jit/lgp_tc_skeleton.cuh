@@ -4,7 +4,7 @@
 //
 // Prepended by lgp_codegen.cpp: lgp_jit_abi.h, #defines LGP_D, LGP_TC_KD
 // (K of the distance GEMM in FP16 halves: 3D + 4 rounded up to 16), LGP_TC_N
-// (right-hand sides per pass: 8, 16 or 32), LGP_TC_NSB (S buffers that fit
+// (right-hand sides per pass: 8, 16, 32 or 64), LGP_TC_NSB (S buffers that fit
 // next to the accumulators in TMEM), LGP_TC_G (chunks per FP32 accumulation
 // group), LGP_TC_STAGES, LGP_TC_FW / P0 / PF (FP32 point features, Periodic
 // block), and the generated lgp_tc_prep_point() / lgp_tc_k() / lgp_tc_kf().
@@ -21,8 +21,14 @@
 //   epilogue (8 warps, SIMT): r^2 -> k (the tree, one MUFU.EX2 per exp) ->
 //       FP16 hi/lo split -> tcgen05.st back into TMEM as the A operand of
 //   GEMM2 (kind::f16, A = P from TMEM as FP16 hi/lo, B = [V_hi ; V_lo] tile
-//       from SMEM, FP16 hi/lo of a power-of-two column scaling, N = 2 x RHS):
-//       D2[128 x 2N] += P_hi.[V_hi V_lo] + P_lo.[V_hi V_lo]  (2 MMAs per 16 columns)
+//       from SMEM, FP16 hi/lo of a power-of-two column scaling):
+//       up to 32 RHS:  D2[128 x 2N] += P_hi.[V_hi V_lo] + P_lo.[V_hi V_lo]
+//                      (2 MMAs per 16 columns, hi / lo columns summed at the drain)
+//       64 RHS:        D2[128 x N] += P_hi.V_hi + P_lo.V_hi + P_hi.V_lo
+//                      (3 MMAs per 16 columns into one accumulator - half the
+//                      TMEM columns; the lo.lo term, 2^-22 relative, dropped as
+//                      in the distance GEMM; 12 instead of 8 MMAs per chunk
+//                      cost 6 % at 16 RHS, hence only where TMEM needs it)
 //   D2 (FP32, TMEM) is drained every LGP_TC_G chunks of a warpgroup into FP64
 //   registers; the two epilogue warpgroups' FP64 sums are combined in a fixed
 //   order and written as this segment's partial (deterministic).
@@ -32,7 +38,9 @@
 // warpgroups 0 / 1 (one MMA-issuing thread sustains ~60-90 cycles per MMA),
 // warps 2..5 / 6..9 = epilogue warpgroups 0 / 1 (even / odd chunks). TMEM:
 // LGP_TC_NSB S buffers of 64 columns (S' in FP32, then P packed FP16 hi | lo
-// in place) + 2 x 2 D2 accumulators of 2N columns.
+// in place) + 2 x 2 D2 accumulators (2N columns, N with 64 RHS). With 64 RHS the FP64 row
+// sums take 128 registers per thread, so the epilogue handles each chunk in
+// two 32-column halves (P of a half packed inside the half's columns).
 //
 // (Measured and dropped, round 1: CTA pairs (cta_group::2, M = 256: 5.1 vs
 // 3.6 ms at cfg4 - MMA instructions are not the binding resource), distance
@@ -53,10 +61,17 @@
 
 #define TC_CH 64
 #define TC_THREADS 384  // 12 warps: producer, 3 MMA issuers, 2 epilogue warpgroups
-#if LGP_TC_N != 8 && LGP_TC_N != 16 && LGP_TC_N != 32
-#error "K1-TC takes 8, 16 or 32 right-hand sides per pass"
+#if LGP_TC_N != 8 && LGP_TC_N != 16 && LGP_TC_N != 32 && LGP_TC_N != 64
+#error "K1-TC takes 8, 16, 32 or 64 right-hand sides per pass"
 #endif
-#define TC_N2 (2 * LGP_TC_N)  // GEMM2 N: V_hi and V_lo rows side by side
+#define TC_KSTACK (LGP_TC_N == 64)                 // cross terms stacked in K (see above)
+#define TC_N2 (TC_KSTACK ? LGP_TC_N : 2 * LGP_TC_N)  // GEMM2 N = D2 columns
+// epilogue round trips per chunk: 64 RHS -> two 32-column halves
+#define TC_HALVES (LGP_TC_N == 64 ? 2 : 1)
+// TMEM column (within an S buffer) of the FP16x2 hi / lo words of the
+// contraction's K step kk (16 chunk columns)
+#define TC_PHI(kk) (TC_HALVES == 1 ? 8u * (kk) : 32u * ((kk) >> 1) + 8u * ((kk) & 1))
+#define TC_PLO(kk) (TC_PHI(kk) + (TC_HALVES == 1 ? 32u : 16u))
 #define TC_V_HALFS (LGP_TC_N * TC_CH)
 // row / column operand tiles (FP16, UMMA K-major canonical layout)
 #define TC_A1_BYTES (128 * LGP_TC_KD * 2)
@@ -269,6 +284,16 @@ __device__ __forceinline__ void lgp_tmem_st32s2(unsigned taddr, const unsigned* 
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%"
       "14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
       LGP_W8S2(v, 0), LGP_W8S2(v, 16), LGP_W8S2(v, 32), LGP_W8S2(v, 48)
+      : "memory");
+}
+
+#define LGP_W4S2(a, o) "r"(a[o + 0]), "r"(a[o + 2]), "r"(a[o + 4]), "r"(a[o + 6])
+// 16 columns from v[0], v[2], ..., v[30]
+__device__ __forceinline__ void lgp_tmem_st16s2(unsigned taddr, const unsigned* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16};" ::"r"(taddr),
+      LGP_W4S2(v, 0), LGP_W4S2(v, 8), LGP_W4S2(v, 16), LGP_W4S2(v, 24)
       : "memory");
 }
 
@@ -513,15 +538,18 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
         if (first && gi >= 2) lgp_mbar_wait(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
         lgp_tc_fence_after();
         const int s = c % LGP_TC_STAGES;
-        // B = [V_hi ; V_lo]
+        // B = V_hi (rows 0..N-1 of the staged V tile) and V_lo (rows N..2N-1)
         const unsigned long long v_d = dv + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4) + (TC_B1_BYTES >> 4);
         const unsigned d = T_D2(w, b);
         const unsigned p = T_SB(q);
 #pragma unroll
         for (int kk = 0; kk < TC_CH / 16; ++kk) {
           const unsigned o = 16u * kk;
-          lgp_mma_f16_ts(d, p + 8u * kk, v_d + o, idesc2, (first && kk == 0) ? 0u : 1u);
-          lgp_mma_f16_ts(d, p + 32u + 8u * kk, v_d + o, idesc2, 1u);
+          lgp_mma_f16_ts(d, p + TC_PHI(kk), v_d + o, idesc2, (first && kk == 0) ? 0u : 1u);
+          lgp_mma_f16_ts(d, p + TC_PLO(kk), v_d + o, idesc2, 1u);
+#if TC_KSTACK
+          lgp_mma_f16_ts(d, p + TC_PHI(kk), v_d + ((unsigned)(LGP_TC_N * 128) >> 4) + o, idesc2, 1u);
+#endif
         }
         lgp_mma_commit(BAR(B_SEMPTY(s)));
         lgp_mma_commit(BAR(B_PEMPTY(q)));
@@ -550,9 +578,10 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       const int b = gi & 1;
       lgp_mbar_wait(BAR(B_D2FULL(w, b)), (gi >> 1) & 1);
       lgp_tc_fence_after();
-      // columns 0..N-1: P.V_hi, N..2N-1: P.V_lo
+      // column i: RHS i of the pass (up to 32 RHS: P.V_hi in columns
+      // 0..N-1, P.V_lo in N..2N-1, both added)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < (TC_KSTACK ? 1 : 2); ++h) {
 #if LGP_TC_N == 8
         unsigned v[8];
         lgp_tmem_ld8(T_D2(w, b) + lanes + 8u * h, v);
@@ -578,14 +607,8 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
     for (int k = 0; k < nloc; ++k) {
       const int q = w + 2 * (k % TC_NSBW);
       const unsigned sb = T_SB(q) + lanes;
-      unsigned s[64];
       lgp_mbar_wait(BAR(B_S1FULL(q)), (k / TC_NSBW) & 1);
       lgp_tc_fence_after();
-      // all 64 columns in one round trip; P overwrites S' in the same
-      // registers: s[2m] = FP16x2 hi of entries (2m, 2m+1), s[2m+1] = lo
-      lgp_tmem_ld32p(sb, s);
-      lgp_tmem_ld32p(sb + 32u, s + 32);
-      lgp_tmem_wait_ld();
 #if LGP_TC_PF
       // column Periodic features of this chunk, staged with its B tile (the
       // stage is released only after this chunk's contraction)
@@ -597,6 +620,13 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
 #else
 #define TC_KJ(x, pxv, j) lgp_tc_k((x), a, (pxv))
 #endif
+#if TC_HALVES == 1
+      // all 64 columns in one round trip; P overwrites S' in the same
+      // registers: s[2m] = FP16x2 hi of entries (2m, 2m+1), s[2m+1] = lo
+      unsigned s[64];
+      lgp_tmem_ld32p(sb, s);
+      lgp_tmem_ld32p(sb + 32u, s + 32);
+      lgp_tmem_wait_ld();
 #pragma unroll
       for (int m = 0; m < 32; ++m) {
         const int px = (m & 7) < (LGP_TC_POLY + 1) / 2 ? 1 : 0;
@@ -605,9 +635,30 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
         const float k1 = TC_KJ(LGP_TC_CLAMP(__uint_as_float(s[2 * m + 1])), px1, 2 * m + 1);
         lgp_split_f16x2(k0, k1, s[2 * m], s[2 * m + 1]);
       }
-#undef TC_KJ
       lgp_tmem_st32s2(sb, s);            // hi pairs -> columns 0..31
       lgp_tmem_st32s2(sb + 32u, s + 1);  // lo pairs -> columns 32..63
+#else
+      // two 32-column halves (registers: the FP64 row sums of 64 RHS take
+      // 128); half h's P words stay inside its own columns: hi -> 32h + 0..15,
+      // lo -> 32h + 16..31 (the next half's S' columns are not touched)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        unsigned s[32];
+        lgp_tmem_ld32p(sb + 32u * h, s);
+        lgp_tmem_wait_ld();
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          const int px = (m & 7) < (LGP_TC_POLY + 1) / 2 ? 1 : 0;
+          const int px1 = (m & 7) < LGP_TC_POLY / 2 ? 1 : 0;
+          const float k0 = TC_KJ(LGP_TC_CLAMP(__uint_as_float(s[2 * m])), px, 32 * h + 2 * m);
+          const float k1 = TC_KJ(LGP_TC_CLAMP(__uint_as_float(s[2 * m + 1])), px1, 32 * h + 2 * m + 1);
+          lgp_split_f16x2(k0, k1, s[2 * m], s[2 * m + 1]);
+        }
+        lgp_tmem_st16s2(sb + 32u * h, s);             // hi pairs -> columns 32h + 0..15
+        lgp_tmem_st16s2(sb + 32u * h + 16u, s + 1);   // lo pairs -> columns 32h + 16..31
+      }
+#endif
+#undef TC_KJ
       lgp_tmem_wait_st();
       lgp_tc_fence_before();
       __syncwarp();

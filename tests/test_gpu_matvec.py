@@ -358,13 +358,14 @@ def test_tensor_core_tuning_parity(gpu_ctx, monkeypatch, env):
     assert rel_l2(got, O.matvec(O.parse_tree(expr), x, 0.1, V)) <= TOL
 
 
-@pytest.mark.parametrize("t", [8, 9, 16, 17, 32, 33, 64, 100])
+@pytest.mark.parametrize("t", [8, 9, 16, 17, 32, 33, 64, 65, 100])
 @pytest.mark.parametrize("expr,d", [("(rbf 0.5)", 8), ("(matern32 0.5)", 8),
                                     ("(+ (scale 1.0 (rbf 0.5)) (scale 1.0 (periodic 1.0 1.0)))", 2)])
 def test_tensor_core_rhs_widths(gpu_ctx, t, expr, d):
-    """K1-TC runs 8, 16 or 32 right-hand sides per pass (GEMM2 N = 16 / 32 /
-    64; t > 32 in passes of 32): every width, ragged t included, meets the
-    bar against the oracle, with Gaussian and +-1 columns."""
+    """K1-TC runs 8, 16, 32 or 64 right-hand sides per pass (GEMM2 N = RHS,
+    three hi/lo cross terms; t > 64 in passes of 64): every width, ragged t
+    included, meets the bar against the oracle, with Gaussian and +-1
+    columns."""
     rng = np.random.default_rng(t)
     n = 2500
     x = rng.random((n, d))
