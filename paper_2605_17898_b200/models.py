@@ -87,7 +87,15 @@ def _resolve_strategy(strategy, n, d, kernel):
 
 def gp_fit(x, y, kernel, noise, strategy="auto", *, cg_config=None, grid_size=None, ctx=None):
     """Fit an exact GP with the device CG solver (models.py:143-200). ``ctx``:
-    the library context (GPU / stream) to run on, default the process's."""
+    the library context (GPU / stream) to run on, default the process's.
+
+    Only the matrix-free CG path is provided: ``strategy`` must be ``"cg"``,
+    or ``"auto"`` where the reference resolves it to CG (N > 4000 and not a
+    1-D stationary kernel, models.py:130-140). The reference's Cholesky and
+    SKI strategies (the default ``"auto"`` for N <= 4000) raise
+    ``NotImplementedError`` rather than fall back to a CPU path. Unlike the
+    reference, N <= 2048 also uses the matrix-free operator (the reference
+    switches to a dense Gram there, models.py:174-182)."""
     x = as_matrix(x, "X")
     y = as_vector(y, "y")
     n, d = x.shape
