@@ -736,20 +736,20 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
       }
       vec::cg1_update(ctx, b.x, b.r, b.p, b.ap, n, part1, cnt1, it, max_iter, b.s);
     } else {
-    if (split) {
-      // this rank's pair share over all rows (noise term on rank 0 only), then
-      // the sum over ranks: one all-reduce of n doubles per iteration
-      op.run(b.p, b.ap, ctx->rank == 0 ? noise : 0.0, ctx->rank == 0 ? b.p : nullptr, b.s.done);
-      comm_allreduce_sum_inplace(ctx->comm, b.ap, (size_t)n, ctx->stream);
-    } else {
-      op.run(b.p, b.ap + r0 * t, noise, b.p + r0 * t, b.s.done);
-      if (ctx->sharded()) comm_allgather_inplace(ctx->comm, b.ap, (size_t)S * t, ctx->stream);
-    }
-    vec::dot_partial(ctx, b.p, b.ap, n, t, b.part, b.s.done);
-    vec::cg_fin_pap(ctx, b.part, nblk, t, b.s);
-    vec::cg_update_xr(ctx, b.x, b.r, b.p, b.ap, n, t, b.s, b.part);
-    vec::cg_fin_rs(ctx, b.part, nblk, t, it, max_iter, b.s);
-    vec::cg_update_p(ctx, b.p, b.r, n, t, b.s);
+      if (split) {
+        // this rank's pair share over all rows (noise term on rank 0 only), then
+        // the sum over ranks: one all-reduce of n doubles per iteration
+        op.run(b.p, b.ap, ctx->rank == 0 ? noise : 0.0, ctx->rank == 0 ? b.p : nullptr, b.s.done);
+        comm_allreduce_sum_inplace(ctx->comm, b.ap, (size_t)n, ctx->stream);
+      } else {
+        op.run(b.p, b.ap + r0 * t, noise, b.p + r0 * t, b.s.done);
+        if (ctx->sharded()) comm_allgather_inplace(ctx->comm, b.ap, (size_t)S * t, ctx->stream);
+      }
+      vec::dot_partial(ctx, b.p, b.ap, n, t, b.part, b.s.done);
+      vec::cg_fin_pap(ctx, b.part, nblk, t, b.s);
+      vec::cg_update_xr(ctx, b.x, b.r, b.p, b.ap, n, t, b.s, b.part);
+      vec::cg_fin_rs(ctx, b.part, nblk, t, it, max_iter, b.s);
+      vec::cg_update_p(ctx, b.p, b.r, n, t, b.s);
     }
     if (it % check_every == 0 || it == max_iter) done_h = poll.check();
   }
