@@ -272,7 +272,7 @@ void MatvecOp::prepare() {
     }
   }
   if (!tcsym && allow_tc) {
-    plan = make_tc_plan(k->tree, rows->d, t, flags);
+    plan = make_tc_plan(k->tree, rows->d, std::max(t, tc_t_hint), flags);
     // many Periodic features (> 24 per point) spill in the multi-RHS
     // epilogue: the SIMT kernel is faster there (2 leaves at D = 8: 2.97 vs
     // 3.59 ms; tools/periodic_pf_sweep.py); the t = 1 symmetric kernel still wins
@@ -310,6 +310,7 @@ void MatvecOp::prepare() {
   }
   if (const char* e = std::getenv("LGP_SEGMENTS")) best = std::max(1, std::min(n_tiles, atoi(e)));
   tiles_per_seg = ceil_div(n_tiles, best);
+  if (tiles_per_seg_hint > 0) tiles_per_seg = std::min(n_tiles, tiles_per_seg_hint);
   n_seg = ceil_div(n_tiles, tiles_per_seg);
 
   if (!tcsym) partial = (double*)ctx->scratch_get(tag + ".part", (size_t)n_seg * n_pass * n_rows_pad * tb * 8);
@@ -686,6 +687,19 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
     op.prepare();
   }
   const bool split = op.rank_split && op.tcsym;
+  // multi-pass multi-RHS CG on one rank: drop converged columns from the K1
+  // passes as they converge (LGP_CG_NO_COMPACT=1 keeps every column)
+  const bool compact = !ctx->sharded() && t > 1 && op.plan.tc && t > op.plan.tc_n &&
+                       !std::getenv("LGP_CG_NO_COMPACT");
+  int t_run = t;
+  MatvecOp opc;
+  int* cmap = nullptr;
+  double *pc = nullptr, *apc = nullptr;
+  if (compact) {
+    cmap = (int*)ctx->scratch_get("cg.cmap", (size_t)t * sizeof(int));
+    pc = (double*)ctx->scratch_get("cg.pc", (size_t)n_alloc * t * 8);
+    apc = (double*)ctx->scratch_get("cg.apc", (size_t)n_alloc * t * 8);
+  }
 
   vec::dot_partial(ctx, B_dev, B_dev, n, t, b.part, nullptr);
   vec::dot_final(ctx, b.part, nblk, t, b.bb, nullptr);
@@ -741,6 +755,11 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
         // the sum over ranks: one all-reduce of n doubles per iteration
         op.run(b.p, b.ap, ctx->rank == 0 ? noise : 0.0, ctx->rank == 0 ? b.p : nullptr, b.s.done);
         comm_allreduce_sum_inplace(ctx->comm, b.ap, (size_t)n, ctx->stream);
+      } else if (t_run < t) {
+        // the still-active columns only (see the compaction below)
+        vec::gather_cols(ctx, b.p, n, t, cmap, t_run, pc, b.s.done);
+        opc.run(pc, apc, noise, pc, b.s.done);
+        vec::scatter_cols(ctx, apc, n, t_run, cmap, t, b.ap, b.s.done);
       } else {
         op.run(b.p, b.ap + r0 * t, noise, b.p + r0 * t, b.s.done);
         if (ctx->sharded()) comm_allgather_inplace(ctx->comm, b.ap, (size_t)S * t, ctx->stream);
@@ -752,6 +771,40 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
       vec::cg_update_p(ctx, b.p, b.r, n, t, b.s);
     }
     if (it % check_every == 0 || it == max_iter) done_h = poll.check();
+    if (compact && it % 8 == 0 && !done_h) {
+      // columns converge at different iterations (cfg4 predictive variance:
+      // 608-804): once the active ones fit in fewer K1 passes, run only those
+      // (converged columns are never updated again, so a mask read a few
+      // iterations late is a superset of the active set)
+      std::vector<int> act(t);
+      LGP_CUDA_CHECK(cudaMemcpyAsync(act.data(), b.s.active, t * sizeof(int), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+      LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+      std::vector<int> cols;
+      for (int c = 0; c < t; ++c)
+        if (act[c]) cols.push_back(c);
+      const int tb = op.plan.tc_n;
+      if (!cols.empty() && ceil_div<int>((int)cols.size(), tb) < ceil_div<int>(t_run, tb)) {
+        t_run = (int)cols.size();
+        LGP_CUDA_CHECK(cudaMemcpyAsync(cmap, cols.data(), cols.size() * sizeof(int),
+                                       cudaMemcpyHostToDevice, ctx->stream));
+        opc = MatvecOp{};
+        opc.ctx = ctx;
+        opc.k = k;
+        opc.rows = pts;
+        opc.cols = pts;
+        opc.row0 = 0;
+        opc.n_rows = n;
+        opc.t = t_run;
+        // the same RHS-per-pass kernel and column segments: per-column results
+        // bit-identical to the full pass set
+        opc.tc_t_hint = t;
+        opc.tiles_per_seg_hint = op.tiles_per_seg;
+        opc.allow_tc = true;
+        opc.tag = "cg.mvc";
+        opc.prepare();
+      }
+    }
   }
   poll.drain();
   int status[2] = {0, -1};

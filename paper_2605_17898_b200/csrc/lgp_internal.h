@@ -247,6 +247,8 @@ struct MatvecOp {
   Plan plan;
   Module* mod = nullptr;
   bool allow_tc = false;  // may use the tensor-core K1 (matvec API, Lanczos; not CG)
+  int tc_t_hint = 0;      // pick K1-TC's RHS per pass as for max(t, this)
+  int tiles_per_seg_hint = 0;  // column tiles per segment (0: fill whole waves)
   bool sym = false;       // square operator on one rank: symmetric block-pair kernel
   bool tcsym = false;     // square operator, t = 1, one rank: symmetric tensor-core kernel
   // multi-rank CG: every rank evaluates its share of the symmetric pair items
@@ -370,6 +372,11 @@ void tcsym_epilogue_cg(Context* c, const double* rowpart, const double* colpart,
                        double scale, double noise, const double* p, double* out, double* part,
                        unsigned* counter, CgState s);
 int cg1_blocks(int64_t n);
+// dst[i][k] = src[i][map[k]] for k < t_run (src n x t) / dst[i][map[k]] = src[i][k]
+void gather_cols(Context* c, const double* src, int64_t n, int t, const int* map, int t_run,
+                 double* dst, const int* done);
+void scatter_cols(Context* c, const double* src, int64_t n, int t_run, const int* map, int t,
+                  double* dst, const int* done);
 void cg1_pap(Context* c, const double* p, const double* ap, int64_t n, double* part,
              unsigned* counter, CgState s);
 void cg1_update(Context* c, double* x, double* r, const double* p, const double* ap, int64_t n,

@@ -561,6 +561,35 @@ __global__ void __launch_bounds__(256) k_cg1_update(double* __restrict__ x, doub
   }
 }
 
+// --------------------------------------- column compaction (multi-RHS CG)
+// dst[i][k] = src[i][map[k]] (k < t_run) and back: the multi-RHS CG runs its
+// K1 passes on the still-active columns only
+__global__ void k_gather_cols(const double* __restrict__ src, long long n, int t,
+                              const int* __restrict__ map, int t_run, double* __restrict__ dst,
+                              const int* done) {
+  if (is_done(done)) return;
+  const long long total = n * t_run;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / t_run;
+    const int k = (int)(e - i * t_run);
+    dst[e] = src[i * t + map[k]];
+  }
+}
+
+__global__ void k_scatter_cols(const double* __restrict__ src, long long n, int t_run,
+                               const int* __restrict__ map, int t, double* __restrict__ dst,
+                               const int* done) {
+  if (is_done(done)) return;
+  const long long total = n * t_run;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / t_run;
+    const int k = (int)(e - i * t_run);
+    dst[i * t + map[k]] = src[e];
+  }
+}
+
 // ------------------------------------------------------------- Lanczos
 __global__ void k_lz_init(const double* __restrict__ z, double* __restrict__ q, long long total,
                           int t, const double* zz) {
@@ -1112,6 +1141,18 @@ void cg1_pap(Context* c, const double* p, const double* ap, int64_t n, double* p
 void cg1_update(Context* c, double* x, double* r, const double* p, const double* ap, int64_t n,
                 double* part, unsigned* counter, int it, int max_iter, CgState s) {
   k_cg1_update<<<cg1_blocks(n), 256, 0, c->stream>>>(x, r, p, ap, n, part, counter, it, max_iter, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void gather_cols(Context* c, const double* src, int64_t n, int t, const int* map, int t_run,
+                 double* dst, const int* done) {
+  k_gather_cols<<<grid_for(n * t_run), 256, 0, c->stream>>>(src, n, t, map, t_run, dst, done);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void scatter_cols(Context* c, const double* src, int64_t n, int t_run, const int* map, int t,
+                  double* dst, const int* done) {
+  k_scatter_cols<<<grid_for(n * t_run), 256, 0, c->stream>>>(src, n, t_run, map, t, dst, done);
   LGP_LAUNCH_CHECK(c);
 }
 

@@ -251,3 +251,27 @@ def test_cg_gram_operators_match_cholesky(gpu_ctx, seed, n, d):
                      G.CgConfig(rel_tolerance=1e-11, max_iterations=5 * n))
     assert rel_l2(res.x, want) <= 1e-5
     assert np.max(np.abs(res.x - want)) <= 3e-5
+
+
+def test_multi_rhs_cg_column_compaction(gpu_ctx, monkeypatch):
+    """The multi-RHS CG (predictive variance) drops converged columns from its
+    K1 passes: same per-column iterations, residuals and solutions as keeping
+    every column (LGP_CG_NO_COMPACT=1). 130 columns = 3 passes of 64; three
+    zero columns finish at once (0 iterations) so the rest fit 2 passes from
+    the first check on, and smooth k* columns converge apart from random
+    ones."""
+    x, _ = small_inputs(4000, 8, 61)
+    rng = np.random.default_rng(62)
+    B = rng.standard_normal((4000, 130))
+    B[:, ::7] = G.kernel_eval(G.parse_kernel("(rbf 0.5)"), x, rng.random((19, 8)))
+    B[:, [5, 50, 100]] = 0.0
+    k = G.parse_kernel("(rbf 0.5)")
+    op = G.KernelOperator(k, x, 0.1)
+    X1, it1, r1 = op.cg(B, 1e-8, None)
+    monkeypatch.setenv("LGP_CG_NO_COMPACT", "1")
+    X0, it0, r0 = op.cg(B, 1e-8, None)
+    print(f"\n[compaction] iterations min/max {it1.min()}/{it1.max()}")
+    assert it1.max() > it1.min() + 8  # columns really converge at different iterations
+    np.testing.assert_array_equal(it1, it0)
+    np.testing.assert_array_equal(r1, r0)
+    np.testing.assert_array_equal(X1, X0)
