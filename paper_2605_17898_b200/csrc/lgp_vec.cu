@@ -441,8 +441,19 @@ __device__ bool deposit_last(double val, double* part, unsigned* counter, int nb
 // block size, so kernels of different block sizes sum in the same order
 __device__ double sum_shares(const double* part, int nblk, double* sm) {
   double v = 0.0;
-  if (threadIdx.x < 64)
-    for (int b = threadIdx.x; b < nblk; b += 64) v += __ldcg(part + b);
+  if (threadIdx.x < 64) {
+    // 8 loads in flight per round (in-order issue would otherwise wait out
+    // one L2 round trip per share); the adds keep the index order
+    int b = threadIdx.x;
+    for (; b + 7 * 64 < nblk; b += 8 * 64) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldcg(part + b + 64 * u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v += x[u];
+    }
+    for (; b < nblk; b += 64) v += __ldcg(part + b);
+  }
   return block_sum_fixed(v, sm);
 }
 
