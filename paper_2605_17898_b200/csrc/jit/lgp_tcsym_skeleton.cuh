@@ -22,8 +22,10 @@
 // triangle with R x 2R super-tiles and splits the ones dispatched last into
 // quarters (load balance of the final wave). Rows run outer, chunks inner;
 // inside the CTA
-//   * column partials accumulate in shared memory over the item's row blocks
-//     (each chunk is owned by one epilogue warpgroup, rows in order), and
+//   * column partials accumulate in shared memory over the item's row blocks,
+//     one accumulator per (warp, chunk, column) so no warp waits for another
+//     (each chunk owned by one epilogue warpgroup, rows in order; the 4 warps
+//     combined in a fixed order once per item), and
 //   * row partials of the 4 warpgroups are combined per row block by a
 //     combiner warp (warpgroups in order),
 // so the item writes R x 128 row and 2R x 64 column FP64 partials once:
@@ -48,7 +50,6 @@
 #define TS_F32_BYTES (LGP_TC_PF ? TC_CH * LGP_TC_FW * 4 : 0)  // column Periodic features
 #define TS_STAGE_BYTES (TC_B1_BYTES + TS_VCH_BYTES + TS_F32_BYTES)
 #define TS_A_BYTES (TC_A1_BYTES + 128 * 8)  // row tile + p of its 128 rows
-#define TS_CBUF_DOUBLES (LGP_TS_NWG * 2 * 4 * TC_CH)  // [wg][parity][warp][64]
 #define TS_RBUF_DOUBLES (LGP_TS_NWG * 2 * 128)        // [wg][slot][128]
 #define TS_NBARS (10 + 2 * LGP_TC_STAGES + 2 * LGP_TS_NSB)  // (incl. 2 ticket counters)
 #define TS_NA 3  // row-tile buffers: row u + 2 loads while row u computes
@@ -60,9 +61,9 @@
 #define TSB_SEMPTY(s) (2 * TS_NA + 4 + LGP_TC_STAGES + (s))
 #define TSB_S1FULL(q) (2 * TS_NA + 4 + 2 * LGP_TC_STAGES + (q))
 #define TSB_SFREE(q) (2 * TS_NA + 4 + 2 * LGP_TC_STAGES + LGP_TS_NSB + (q))
-// shared memory: [TS_NA][TS_A_BYTES] | stages | cbuf | rbuf | bars | tslot | colacc [2R][64]
+// shared memory: [TS_NA][TS_A_BYTES] | stages | rbuf | bars | tslot | colacc [4][2R][64]
 #define TS_SMEM_FIXED \
-  (TS_NA * TS_A_BYTES + LGP_TC_STAGES * TS_STAGE_BYTES + 8 * (TS_CBUF_DOUBLES + TS_RBUF_DOUBLES + TS_NBARS) + 16)
+  (TS_NA * TS_A_BYTES + LGP_TC_STAGES * TS_STAGE_BYTES + 8 * (TS_RBUF_DOUBLES + TS_NBARS) + 16)
 
 // FP32 -> FP64 for finite non-negative kernel values without the conversion
 // pipe (F2F.F64.F32 runs at 16/clk/SM): exponent re-bias + mantissa shift
@@ -109,11 +110,11 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
   extern __shared__ __align__(1024) unsigned char ts_smem[];
   unsigned char* abuf = ts_smem;  // [TS_NA][row tile | p rows]
   unsigned char* stg = ts_smem + TS_NA * TS_A_BYTES;
-  double* cbuf = reinterpret_cast<double*>(stg + LGP_TC_STAGES * TS_STAGE_BYTES);
-  double* rbuf = cbuf + TS_CBUF_DOUBLES;
+  double* rbuf = reinterpret_cast<double*>(stg + LGP_TC_STAGES * TS_STAGE_BYTES);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(rbuf + TS_RBUF_DOUBLES);
   unsigned* tslot = reinterpret_cast<unsigned*>(bars + TS_NBARS);
-  double* colacc = reinterpret_cast<double*>(ts_smem + TS_SMEM_FIXED);  // [2R][64]
+  double* colacc = reinterpret_cast<double*>(ts_smem + TS_SMEM_FIXED);  // [warp][2R][64]
+  const int CM = 2 * a.R;  // chunks per item at most
   const unsigned bar0 = lgp_saddr(bars);
 #define TBAR(i) (bar0 + 8u * (unsigned)(i))
 
@@ -230,12 +231,15 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
     const int w = (warp - 2) >> 2;
     const int q4 = warp & 3;
     const int r0 = lane >> 2, cq = lane & 3;
-    // column accumulators of the warpgroup's chunks: entry (c, 16 q4 + lane)
-    // belongs to this thread alone (lanes < 16), rows in order
-    for (int c = c_lo + w; c < c_hi; c += LGP_TS_NWG)
-      if (lane < 16) colacc[(c - c_lo) * TC_CH + 16 * q4 + lane] = 0.0;
     // after the butterfly lane t holds column 8 k + 2 cq + e, k = 2 b4 + b3, e = b2
     const int ccol = 8 * (2 * ((lane >> 4) & 1) + ((lane >> 3) & 1)) + 2 * cq + ((lane >> 2) & 1);
+    // this warp's column accumulators of the warpgroup's chunks: entries
+    // (q4, c, 32 g + ccol) belong to this lane alone, row blocks in order
+    double* cacc = colacc + (size_t)q4 * CM * TC_CH + ccol;
+    for (int c = c_lo + w; c < c_hi; c += LGP_TS_NWG) {
+      cacc[(size_t)(c - c_lo) * TC_CH] = 0.0;
+      cacc[(size_t)(c - c_lo) * TC_CH + 32] = 0.0;
+    }
     int f_row = 0;  // flat chunk index of the row block's first chunk
     int k = 0;      // this warpgroup's chunk counter
     for (int I = I0; I < I1; ++I) {
@@ -281,7 +285,6 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
         const bool diag = dblk && c < 2 * I + 2;
         // diagonal chunks: column offset relative to this thread's first row
         const int dj0 = c * TC_CH - (128 * I + 32 * q4 + r0) + 2 * cq;
-        double* cb = cbuf + ((size_t)(w * 2 + (k & 1)) * 4 + q4) * TC_CH;
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           unsigned sv[2][16];
@@ -333,19 +336,10 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
           lgp_xreduce<4>(cv, 16, (lane & 16) != 0);
           lgp_xreduce<2>(cv, 8, (lane & 8) != 0);
           lgp_xreduce<1>(cv, 4, (lane & 4) != 0);
-          cb[32 * g + ccol] = cv[0];
+          cacc[(size_t)(c - c_lo) * TC_CH + 32 * g] += cv[0];
         }
         __syncwarp();
         if (lane == 0) lgp_mbar_arrive(TBAR(TSB_SEMPTY(s)));  // p chunk read: stage reusable
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + w) : "memory");
-        // column partial of (I, c): warps 0..3 in a fixed order, added to the
-        // chunk's accumulator (row blocks in order)
-        if (lane < 16) {
-          const int j = 16 * q4 + lane;
-          const double* b0 = cbuf + (size_t)(w * 2 + (k & 1)) * 4 * TC_CH;
-          const double sum = ((b0[j] + b0[TC_CH + j]) + b0[2 * TC_CH + j]) + b0[3 * TC_CH + j];
-          colacc[(c - c_lo) * TC_CH + j] += sum;
-        }
       }
       f_row += c_hi - cs;
       // row side: the 4 lanes of a row (lane bits 0, 1) -> lane holds x = 2 b1 + b0
@@ -383,11 +377,16 @@ extern "C" __global__ void __launch_bounds__(TS_THREADS, 1) lgp_matvec_tcsym(con
       }
 #undef TS_KJ
     }
-    // the item's column partials (this thread's entries only)
+    // the item's column partials: the warpgroup's 4 warps in a fixed order
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + w) : "memory");
     if (lane < 16) {
+      const int j = 16 * q4 + lane;
       double* cp = a.colpart + (size_t)crec * TC_CH;
-      for (int c = c_lo + w; c < c_hi; c += LGP_TS_NWG)
-        cp[(size_t)(c - c_lo) * TC_CH + 16 * q4 + lane] = colacc[(c - c_lo) * TC_CH + 16 * q4 + lane];
+      for (int c = c_lo + w; c < c_hi; c += LGP_TS_NWG) {
+        const double* ca = colacc + (size_t)(c - c_lo) * TC_CH + j;
+        cp[(size_t)(c - c_lo) * TC_CH + j] =
+            ((ca[0] + ca[(size_t)CM * TC_CH]) + ca[(size_t)2 * CM * TC_CH]) + ca[(size_t)3 * CM * TC_CH];
+      }
     }
   }
   lgp_tc_fence_before();

@@ -170,8 +170,8 @@ const TsSchedule& ts_schedule(Context* ctx, int n_rb, int n_tiles, int rmax, boo
     int forced = 0;
     if (const char* e = std::getenv("LGP_TS_R")) forced = std::max(1, std::min(rmax, atoi(e)));
     for (int Rc : cands) {
-      if (Rc > rmax) break;
-      if (forced && Rc != forced) continue;
+      if (forced) Rc = forced;  // LGP_TS_R: exactly that R (any value <= rmax)
+      else if (Rc > rmax) break;
       const int64_t nG = ceil_div<int64_t>(n_rb, Rc);
       if (nG * (nG + 1) / 2 > 2000000) continue;
       std::vector<TsRect> rc = ts_items(n_rb, n_tiles, Rc, ctx->sm_count);
@@ -184,9 +184,11 @@ const TsSchedule& ts_schedule(Context* ctx, int n_rb, int n_tiles, int rmax, boo
         R = Rc;
         rects.swap(rc);
       }
+      if (forced) break;
     }
     if (forced) R = forced;
   }
+  if (rects.empty()) throw Error(LGP_E_UNSUPPORTED, "K1-TC-sym: no work items");
   const int n_items = (int)rects.size();
   int item_lo = 0, item_hi = n_items;
   if (rank_split && ctx->world > 1) {
@@ -474,7 +476,7 @@ void MatvecOp::tcsym_kernel(const int* done) {
   std::memcpy(a.kc, plan.tca.kc, sizeof a.kc);
   if (item_hi > item_lo)
     launch(ctx, mod->tcsym, (unsigned)(item_hi - item_lo), 1, 64 + 128 * plan.ts_nwg,
-           plan.smem_tcsym_fixed + (size_t)2 * ts_R * 64 * 8, &a);
+           plan.smem_tcsym_fixed + (size_t)4096 * ts_R, &a);
 }
 
 void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const double* noise_v,

@@ -132,31 +132,42 @@ def test_model_small_matrix_free_branch(gpu_ctx, name):
     assert abs(lml - float(g[f"{name}_lml"])) <= 1e-4 * abs(float(g[f"{name}_lml"]))
 
 
+def _fp64_cg(expr, x, b, tol=1e-8):
+    """The reference algorithm (solvers.py:87-123) on the exact FP64 Gram."""
+    nodes = O.parse_tree(expr)
+    gram = O.gram(nodes, x, x, same=True)
+    gram.flat[:: x.shape[0] + 1] += 0.1
+    return O.cg(lambda v: gram @ v, b, tol)
+
+
 @pytest.mark.parametrize("nwg,r", [("4", ""), ("3", ""), ("4", "1"), ("4", "3")])
 def test_symmetric_tensor_core_cg(gpu_ctx, monkeypatch, nwg, r):
     """The symmetric tensor-core CG matvec (default for D >= 4 r^2 trees)
-    evaluates each unordered pair once: exactly symmetric, so CG matches the
-    symmetric SIMT kernel's (LGP_NO_TCSYM) iteration count and solution, and
-    the matvec meets the 1e-5 bar, for 4 and 3 epilogue warpgroups and forced
-    super-tile sizes (LGP_TS_R; default: the scheduling model's choice)."""
+    evaluates each unordered pair once: exactly symmetric, so CG tracks the
+    reference algorithm on the exact FP64 Gram (iterations, solution), like
+    the symmetric SIMT kernel (LGP_NO_TCSYM) does, for 4 and 3 epilogue
+    warpgroups and forced super-tile sizes (LGP_TS_R; default: the scheduling
+    model's choice); the matvec meets the 1e-5 bar."""
     x, b = small_inputs(3000, 8, 41)
-    k = G.parse_kernel("(scale 1.2 (rbf 0.6))")
+    expr = "(scale 1.2 (rbf 0.6))"
+    k = G.parse_kernel(expr)
+    ref = _fp64_cg(expr, x, b)
     monkeypatch.setenv("LGP_NO_TCSYM", "1")
-    base = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
+    base = G.cg_solve(G.KernelOperator(k, x, 0.1, ctx=_lib.Context(0)), b, G.CgConfig(rel_tolerance=1e-8))
     monkeypatch.delenv("LGP_NO_TCSYM")
     monkeypatch.setenv("LGP_TS_NWG", nwg)
     if r:
         monkeypatch.setenv("LGP_TS_R", r)
     op = G.KernelOperator(k, x, 0.1, ctx=_lib.Context(0))
     res = G.cg_solve(op, b, G.CgConfig(rel_tolerance=1e-8))
-    print(f"\n[tcsym nwg={nwg} R={r or 'auto'}] iterations {res.iterations} vs SIMT-sym {base.iterations}")
-    # rounding-order differences move the count either way; an asymmetric
-    # operator would cost 25-50 % MORE iterations
-    assert abs(res.iterations - base.iterations) <= max(2, 0.03 * base.iterations)
-    assert rel_l2(res.x, base.x) <= 1e-4
+    print(f"\n[tcsym nwg={nwg} R={r or 'auto'}] iterations {res.iterations}, SIMT-sym {base.iterations}, "
+          f"FP64 reference {ref[1]}; x relL2 {rel_l2(res.x, ref[0]):.1e} (SIMT-sym {rel_l2(base.x, ref[0]):.1e})")
+    for it, xs in ((res.iterations, res.x), (base.iterations, base.x)):
+        assert abs(it - ref[1]) <= max(3, 0.05 * ref[1])
+        assert rel_l2(xs, ref[0]) <= 1e-4
     v = np.random.default_rng(5).standard_normal(3000)
-    ref = O.matvec(O.parse_tree(G.format_kernel(k)), x, 0.1, v)
-    assert rel_l2(op(v), ref) <= 1e-5
+    want = O.matvec(O.parse_tree(expr), x, 0.1, v)
+    assert rel_l2(op(v), want) <= 1e-5
 
 
 def test_evidence_optimizer_matches_reference(gpu_ctx):
@@ -179,16 +190,27 @@ def test_evidence_optimizer_matches_reference(gpu_ctx):
 @pytest.mark.parametrize("d,expr", [(4, "(matern52 0.7)"), (40, "(rbf 2.5)"),
                                     (2, "(+ (scale 1.0 (rbf 0.5)) (scale 1.0 (periodic 1.0 1.0)))")])
 def test_symmetric_tensor_core_cg_dims(gpu_ctx, monkeypatch, d, expr):
-    """The default CG matvec for r^2 trees (K1-TC-sym) at the smallest and a
-    large feature dimension: same iterations / solution as the SIMT kernel."""
+    """The default CG matvec for r^2 / Periodic trees (K1-TC-sym) at the
+    smallest and a large feature dimension: iterations and solution track the
+    reference algorithm on the exact FP64 Gram, as the SIMT kernel's do."""
     x, b = small_inputs(2500, d, 43)
     k = G.parse_kernel(expr)
+    ref = _fp64_cg(expr, x, b)
     monkeypatch.setenv("LGP_NO_TCSYM", "1")
-    base = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
+    base = G.cg_solve(G.KernelOperator(k, x, 0.1, ctx=_lib.Context(0)), b, G.CgConfig(rel_tolerance=1e-8))
     monkeypatch.delenv("LGP_NO_TCSYM")
-    res = G.cg_solve(G.KernelOperator(k, x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
-    assert abs(res.iterations - base.iterations) <= max(2, 0.03 * base.iterations)
-    assert rel_l2(res.x, base.x) <= 1e-4
+    res = G.cg_solve(G.KernelOperator(k, x, 0.1, ctx=_lib.Context(0)), b, G.CgConfig(rel_tolerance=1e-8))
+    print(f"\n[tcsym d={d} {expr}] iterations {res.iterations}, SIMT-sym {base.iterations}, FP64 reference "
+          f"{ref[1]}; x relL2 {rel_l2(res.x, ref[0]):.1e} (SIMT-sym {rel_l2(base.x, ref[0]):.1e})")
+    # the RBF + Periodic system at D = 2 is the rounding-sensitive one: its
+    # recurrence residual reaches 1e-8 between 170 and 184 iterations depending
+    # on the summation order alone (super-tile sizes R = 1..8: 178-179; the
+    # default schedule: 170; FP64: 184) while the solution error stays 2e-5
+    # (tools/tcsym_repeat.py)
+    bar = 0.10 if "periodic" in expr else 0.05
+    for it, xs in ((res.iterations, res.x), (base.iterations, base.x)):
+        assert abs(it - ref[1]) <= max(3, bar * ref[1])
+        assert rel_l2(xs, ref[0]) <= 1e-4
 
 
 @pytest.mark.parametrize("expr,d", [("(scale 1.2 (rbf 0.6))", 8),
