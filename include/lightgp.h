@@ -165,6 +165,19 @@ int lgp_cg(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* pts, double nois
            const double* B, int32_t t, double rel_tol, int32_t max_iter, double* X_out,
            int32_t* iters_out, double* final_res_out, uint32_t flags);
 
+/* Multi-shift CG: solves (K + (noise + shifts[e]) I) x_e = b for all e <
+ * n_shifts (<= 64) with ONE matvec per iteration - the shifted systems share
+ * the seed's Krylov space and residual direction (CG-M, Jegerlehner 1996);
+ * each stops on its own recurrence residual (solvers.py:114-119 per solve).
+ * noise: the seed system's (the smallest); shifts[e] >= 0 relative to it.
+ * X_out: n x n_shifts row-major; iters_out / final_res_out: n_shifts. Used
+ * by the optimiser for the 2P + 1 evaluations that differ only in the root
+ * output scale and the noise. */
+int lgp_cg_shifted(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* pts, double noise,
+                   const double* b, int32_t n_shifts, const double* shifts, double rel_tol,
+                   int32_t max_iter, double* X_out, int32_t* iters_out, double* final_res_out,
+                   uint32_t flags);
+
 /* Lanczos with one full CGS re-orthogonalisation pass per step from each
  * column of Z (n x t), all columns in lockstep (solvers.py:126-154).
  * alphas: t x steps, betas: t x (steps-1) (row-major, unused tail = 0),

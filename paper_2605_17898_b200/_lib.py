@@ -50,6 +50,8 @@ _SIGS = {
                       C.c_int),
     "lgp_comm_unique_id": ([C.c_char_p], C.c_int),
     "lgp_comm_allreduce_max": ([_P, C.POINTER(C.c_double), C.c_int32], C.c_int),
+    "lgp_cg_shifted": ([_P, _P, _P, C.c_double, _P, C.c_int32, _D, C.c_double, C.c_int32, _P,
+                        _I32, _D, C.c_uint32], C.c_int),
     "lgp_ctx_create": ([C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_P)], C.c_int),
     "lgp_ctx_destroy": ([_P], C.c_int),
     "lgp_ctx_sync": ([_P], C.c_int),

@@ -549,6 +549,43 @@ int lgp_cg(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* pts, double nois
   API_END
 }
 
+int lgp_cg_shifted(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* pts, double noise,
+                   const double* b, int32_t n_shifts, const double* shifts, double rel_tol,
+                   int32_t max_iter, double* X_out, int32_t* iters_out, double* final_res_out,
+                   uint32_t flags) {
+  API_BEGIN
+  require(ctx && k && pts && b && shifts && X_out && iters_out && final_res_out, LGP_E_ARG,
+          "null argument");
+  require(n_shifts >= 1 && n_shifts <= 64, LGP_E_ARG, "n_shifts must be in [1, 64]");
+  require(rel_tol > 0.0, LGP_E_ARG, "rel_tolerance must be positive");
+  require(std::isfinite(noise) && noise >= 0.0, LGP_E_ARG, "noise must be finite and nonnegative");
+  for (int e = 0; e < n_shifts; ++e)
+    require(std::isfinite(shifts[e]) && shifts[e] >= 0.0, LGP_E_ARG,
+            "shifts must be finite and nonnegative (the seed has the smallest noise)");
+  const int64_t n = pts->n;
+  require(n >= 1, LGP_E_DIM, "need at least one point");
+  std::lock_guard<std::recursive_mutex> g(ctx->mu);
+  ctx->activate();
+  const int64_t S = (n + ctx->world - 1) / ctx->world;
+  const int64_t n_alloc = S * ctx->world;
+  const double* Bd = stage_in(ctx, "api.B", b, n, 1, n_alloc, flags);
+  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(b, (size_t)n, "b");
+  double* xs = (double*)ctx->scratch_get("api.Xs", (size_t)n_alloc * n_shifts * 8);
+  CgShifts sh;
+  sh.n = n_shifts;
+  sh.sig = shifts;
+  sh.xs_dev = xs;
+  sh.iters = iters_out;
+  sh.res = final_res_out;
+  double* xd = nullptr;
+  int32_t it_seed = 0;
+  double res_seed = 0.0;
+  cg_device(ctx, k, pts, noise, Bd, 1, rel_tol, max_iter, &xd, &it_seed, &res_seed, &sh);
+  stage_out(ctx, X_out, xs, (size_t)n * n_shifts * 8, flags);
+  LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
 int lgp_lanczos(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* pts, double noise,
                 const double* Z, int32_t t, int32_t steps, double* alphas, double* betas,
                 int32_t* steps_out, uint32_t flags) {

@@ -642,7 +642,7 @@ static CgBuffers cg_buffers(Context* ctx, int64_t n_alloc, int t, int nblk) {
 // device in the returned buffers' x; iterations / residuals copied to host.
 void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double noise,
                const double* B_dev, int t, double rel_tol, int max_iter, double** x_dev,
-               int32_t* iters_out, double* res_out) {
+               int32_t* iters_out, double* res_out, const CgShifts* shifts) {
   const int64_t n = pts->n;
   int64_t r0 = 0, r1 = n;
   lgp_partition(n, ctx->world, ctx->rank, &r0, &r1);
@@ -706,6 +706,19 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   vec::dot_partial(ctx, B_dev, B_dev, n, t, b.part, nullptr);
   vec::dot_final(ctx, b.part, nblk, t, b.bb, nullptr);
   vec::cg_init(ctx, B_dev, b.x, b.r, b.p, n, t, rel_tol, b.bb, b.s);
+  // shifted systems on the seed's Krylov space (t = 1): two vectors each
+  const int nsh = shifts ? shifts->n : 0;
+  double *xs = nullptr, *ps = nullptr, *sig = nullptr;
+  vec::CgShiftState* sst = nullptr;
+  if (nsh > 0) {
+    if (t != 1 || nsh > vec::kMaxShifts) throw Error(LGP_E_ARG, "shifted CG: one right-hand side, <= 64 shifts");
+    ps = (double*)ctx->scratch_get("cg.sh.p", (size_t)n_alloc * nsh * 8);
+    sig = (double*)ctx->scratch_get("cg.sh.sig", (size_t)nsh * 8);
+    sst = (vec::CgShiftState*)ctx->scratch_get("cg.sh.state", 2 * sizeof(vec::CgShiftState));
+    xs = shifts->xs_dev;
+    LGP_CUDA_CHECK(cudaMemcpyAsync(sig, shifts->sig, (size_t)nsh * 8, cudaMemcpyHostToDevice, ctx->stream));
+    vec::cg_shift_init(ctx, B_dev, n, nsh, xs, ps, sst);
+  }
 
   // host-side stop checks: every iteration for large operators, else in
   // batches (kernels after convergence early-exit on the device flag)
@@ -751,6 +764,7 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
                                op.plan.root_scale, noise, b.p, b.ap, part1, cnt1, b.s);
       }
       vec::cg1_update(ctx, b.x, b.r, b.p, b.ap, n, part1, cnt1, it, max_iter, b.s);
+      if (nsh > 0) vec::cg_shift(ctx, xs, ps, b.r, n, nsh, sig, sst, b.s, it);
     } else {
       if (split) {
         // this rank's pair share over all rows (noise term on rank 0 only), then
@@ -770,6 +784,7 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
       vec::cg_fin_pap(ctx, b.part, nblk, t, b.s);
       vec::cg_update_xr(ctx, b.x, b.r, b.p, b.ap, n, t, b.s, b.part);
       vec::cg_fin_rs(ctx, b.part, nblk, t, it, max_iter, b.s);
+      if (nsh > 0) vec::cg_shift(ctx, xs, ps, b.r, n, nsh, sig, sst, b.s, it);
       vec::cg_update_p(ctx, b.p, b.r, n, t, b.s);
     }
     if (it % check_every == 0 || it == max_iter) done_h = poll.check();
@@ -816,6 +831,17 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
                                  ctx->stream));
   LGP_CUDA_CHECK(cudaMemcpyAsync(res_out, b.s.res, t * sizeof(double), cudaMemcpyDeviceToHost,
                                  ctx->stream));
+  if (nsh > 0) {
+    // the state the iteration after the seed's last one would read
+    int last = 0;
+    LGP_CUDA_CHECK(cudaMemcpyAsync(&last, b.s.iters, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    const vec::CgShiftState* fin = sst + ((last + 1) & 1);
+    LGP_CUDA_CHECK(cudaMemcpyAsync(shifts->iters, fin->iters, nsh * sizeof(int), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+    LGP_CUDA_CHECK(cudaMemcpyAsync(shifts->res, fin->res, nsh * sizeof(double), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+  }
   LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
   if (status[0] != 0)
     throw Error(LGP_E_NOT_SPD, "CG breakdown: p.A.p is not positive (column " +

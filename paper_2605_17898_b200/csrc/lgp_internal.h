@@ -302,9 +302,19 @@ struct DonePoller {
 };
 std::pair<cudaEvent_t, cudaEvent_t> k1_event_begin(Context* ctx);
 void k1_event_end(Context* ctx, std::pair<cudaEvent_t, cudaEvent_t> ev);
+// shifted systems riding on a single-RHS CG (lgp_cg_shifted): solutions of
+// (K + (noise + sig[e]) I) x_e = b, sig[e] >= 0 (host array), into xs_dev
+// (n x n_sh, device); per-shift iterations / residuals to the host arrays
+struct CgShifts {
+  int n = 0;
+  const double* sig = nullptr;
+  double* xs_dev = nullptr;
+  int32_t* iters = nullptr;
+  double* res = nullptr;
+};
 void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double noise,
                const double* B_dev, int t, double rel_tol, int max_iter, double** x_dev,
-               int32_t* iters_out, double* res_out);
+               int32_t* iters_out, double* res_out, const CgShifts* shifts = nullptr);
 void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, double noise,
                     const double* Z_dev, int t, int steps, double* alphas, double* betas,
                     int32_t* steps_out);
@@ -359,6 +369,18 @@ struct CgState {
   int* done;       // [1]
   int* bad_col;    // [1]
 };
+// multi-shift CG (see lgp_vec.cu): per-shift scalars, double-buffered by
+// iteration parity
+constexpr int kMaxShifts = 64;
+struct CgShiftState {
+  double z[kMaxShifts], zm1[kMaxShifts], res[kMaxShifts];
+  double am1, bm1;  // the seed's alpha_{k-1}, beta_{k-1}
+  int active[kMaxShifts], iters[kMaxShifts];
+};
+void cg_shift_init(Context* c, const double* b, int64_t n, int nsh, double* xs, double* ps,
+                   CgShiftState* st);
+void cg_shift(Context* c, double* xs, double* ps, const double* r, int64_t n, int nsh,
+              const double* sig, CgShiftState* st, CgState s, int it);
 void cg_init(Context* c, const double* b, double* x, double* r, double* p, int64_t n, int t,
              double rel_tol, const double* bb_final, CgState s);
 void cg_fin_pap(Context* c, const double* part, int nblk, int t, CgState s);

@@ -572,6 +572,105 @@ __global__ void __launch_bounds__(256) k_cg1_update(double* __restrict__ x, doub
   }
 }
 
+// ------------------------------------------------ multi-shift CG (CG-M)
+// (K + (noise + sig_e) I) x_e = b for all e at one matvec per iteration:
+// the shifted systems' residuals stay collinear with the seed's,
+// r_e = zeta_e r, so each needs only its own scalars and two vectors
+// (Jegerlehner 1996). With the seed's CG coefficients alpha_k, beta_k:
+//   zeta_{k+1} = zeta_k zeta_{k-1} a_{k-1} /
+//                (zeta_{k-1} a_{k-1} (1 + a_k sig) + a_k b_{k-1} (zeta_{k-1} - zeta_k))
+//   a^e_k = a_k zeta_{k+1} / zeta_k,   b^e_k = b_k (zeta_{k+1} / zeta_k)^2
+//   x^e += a^e_k p^e;   p^e = zeta_{k+1} r_{k+1} + b^e_k p^e
+// stop when |zeta_{k+1}| ||r_{k+1}|| <= tol ||b|| (the shifted system's own
+// recurrence residual: the reference's per-solve rule, solvers.py:114-119).
+// State double-buffered by iteration parity (every block reads [it & 1],
+// block 0 writes [(it + 1) & 1]).
+__global__ void k_cg_shift_init(const double* __restrict__ b, long long n, int nsh,
+                                double* __restrict__ xs, double* __restrict__ ps, CgShiftState* st) {
+  const long long total = n * nsh;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    xs[e] = 0.0;
+    ps[e] = b[e / nsh];
+  }
+  if (blockIdx.x == 0) {
+    CgShiftState* c = st + 1;  // the state the first iteration (it = 1) reads
+    for (int e = threadIdx.x; e < nsh; e += blockDim.x) {
+      c->z[e] = 1.0;
+      c->zm1[e] = 1.0;
+      c->active[e] = 1;
+      c->iters[e] = 0;
+      c->res[e] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+      c->am1 = 1.0;
+      c->bm1 = 0.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_cg_shift(double* __restrict__ xs, double* __restrict__ ps,
+                                                  const double* __restrict__ r, long long n, int nsh,
+                                                  const double* __restrict__ sig, CgShiftState* st,
+                                                  CgState s, int it) {
+  __shared__ double sa[kMaxShifts], sb[kMaxShifts], sz[kMaxShifts];
+  __shared__ int sact[kMaxShifts];
+  // the seed finished at an earlier iteration: nothing left to apply
+  if (*s.done && s.iters[0] != it) return;
+  const bool seed_done = *s.done != 0;  // (then s.iters[0] == it: its last iteration)
+  const CgShiftState* cur = st + (it & 1);
+  CgShiftState* nxt = st + ((it + 1) & 1);
+  const double ak = s.step[0];
+  const double bk = seed_done ? 0.0 : s.beta[0];
+  const double nrm = seed_done ? s.res[0] : sqrt(s.rs[0]);  // ||r_{k+1}|| of the seed
+  for (int e = threadIdx.x; e < nsh; e += blockDim.x) {
+    const int act = cur->active[e];
+    const double zk = cur->z[e], zkm1 = cur->zm1[e];
+    double zn = zk, a = 0.0, be = 0.0;
+    if (act) {
+      const double den = zkm1 * cur->am1 * (1.0 + ak * sig[e]) + ak * cur->bm1 * (zkm1 - zk);
+      zn = zk * zkm1 * cur->am1 / den;
+      a = ak * (zn / zk);
+      be = bk * ((zn / zk) * (zn / zk));
+    }
+    sa[e] = a;
+    sb[e] = be;
+    sz[e] = zn;
+    sact[e] = act;
+    if (blockIdx.x == 0) {
+      nxt->z[e] = zn;
+      nxt->zm1[e] = zk;
+      int a2 = act, iters = cur->iters[e];
+      double res = cur->res[e];
+      if (act) {
+        const double rn = fabs(zn) * nrm;
+        if (rn <= s.tol[0] || seed_done) {  // converged, or the seed (slowest) stopped
+          a2 = 0;
+          iters = it;
+          res = rn;
+        }
+      }
+      nxt->active[e] = a2;
+      nxt->iters[e] = iters;
+      nxt->res[e] = res;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    nxt->am1 = ak;
+    nxt->bm1 = bk;
+  }
+  __syncthreads();
+  const long long total = n * nsh;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(q % nsh);
+    if (!sact[e]) continue;
+    const double pv = ps[q];
+    xs[q] = __dadd_rn(xs[q], __dmul_rn(sa[e], pv));
+    ps[q] = __dadd_rn(__dmul_rn(pv, sb[e]), __dmul_rn(sz[e], r[q / nsh]));
+  }
+}
+
 // --------------------------------------- column compaction (multi-RHS CG)
 // dst[i][k] = src[i][map[k]] (k < t_run) and back: the multi-RHS CG runs its
 // K1 passes on the still-active columns only
@@ -1152,6 +1251,18 @@ void cg1_pap(Context* c, const double* p, const double* ap, int64_t n, double* p
 void cg1_update(Context* c, double* x, double* r, const double* p, const double* ap, int64_t n,
                 double* part, unsigned* counter, int it, int max_iter, CgState s) {
   k_cg1_update<<<cg1_blocks(n), 256, 0, c->stream>>>(x, r, p, ap, n, part, counter, it, max_iter, s);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void cg_shift_init(Context* c, const double* b, int64_t n, int nsh, double* xs, double* ps,
+                   CgShiftState* st) {
+  k_cg_shift_init<<<grid_for(n * nsh), 256, 0, c->stream>>>(b, n, nsh, xs, ps, st);
+  LGP_LAUNCH_CHECK(c);
+}
+
+void cg_shift(Context* c, double* xs, double* ps, const double* r, int64_t n, int nsh,
+              const double* sig, CgShiftState* st, CgState s, int it) {
+  k_cg_shift<<<grid_for(n * nsh), 256, 0, c->stream>>>(xs, ps, r, n, nsh, sig, st, s, it);
   LGP_LAUNCH_CHECK(c);
 }
 

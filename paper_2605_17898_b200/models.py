@@ -287,17 +287,42 @@ def optimize_hyperparams(objective, p0, config):
     return tracked(best_p), trace
 
 
+def _peel_root_scale(kernel):
+    """(c, inner): kernel = c * inner for the chain of Scale nodes at the root
+    (c = 1 without one)."""
+    from .kernels import Scale
+
+    c = 1.0
+    while isinstance(kernel, Scale):
+        c *= float(kernel.outputscale)
+        kernel = kernel.child
+    return c, kernel
+
+
 class _EvidenceObjective:
     """q -> log marginal likelihood of gp_fit(x, y, *unflatten_model_params(
-    kernel, q), "cg"). ``batch(qs)`` evaluates several parameter vectors
-    concurrently: one host thread and one library context (own CUDA stream)
-    per worker, so the small CG / Lanczos kernels of different evaluations
-    overlap on the GPU; every value is bit-identical to a sequential call."""
+    kernel, q), "cg"). ``batch(qs)`` evaluates several parameter vectors at
+    once (an optimiser step's 2P + 1 points):
 
-    def __init__(self, x, y, kernel, cg_config, seed, workers):
+    * points whose kernels differ only in the root output scale c and whose
+      noise differs (centre, +-scale, +-noise) share ONE operator family
+      c (K1 + lam I), lam = noise / c: their fits are one multi-shift CG on K1
+      (lgp_cg_shifted: one matvec per iteration for all of them) and their
+      log-dets one device Lanczos run (shift / scale invariance,
+      solvers.slq_logdet_shifted) - SURVEY.md §8f row 3;
+    * the other points (e.g. +-lengthscale) are single evaluations;
+    * groups / singletons run concurrently, one host thread and one library
+      context (own CUDA stream) per worker.
+
+    A fused value agrees with the separate evaluation to the CG's rounding
+    (~1e-10 relative, tests/test_gpu_solvers.py); ``fuse_shifts=False`` gives
+    bit-identical separate evaluations."""
+
+    def __init__(self, x, y, kernel, cg_config, seed, workers, fuse_shifts=True):
         self.x, self.y, self.kernel = x, y, kernel
         self.cg_config, self.seed = cg_config, seed
         self.workers = workers
+        self.fuse_shifts = fuse_shifts
         self._pool = None
         self._ctx = threading.local()
 
@@ -306,41 +331,96 @@ class _EvidenceObjective:
         st = gp_fit(self.x, self.y, k, noise, "cg", cg_config=self.cg_config, ctx=ctx)
         return log_marginal_likelihood(st, seed=self.seed)
 
+    def _eval_group(self, qs, ctx=None):
+        """Log marginal likelihoods of points that share K1 (see the class
+        doc); one value or exception per point."""
+        from .solvers import _ShiftFallback, slq_logdet_shifted
+
+        mem = []
+        for q in qs:
+            k, noise = unflatten_model_params(self.kernel, q)
+            mem.append((_peel_root_scale(k), _check_noise(noise)))
+        k1 = mem[0][0][1]
+        c = np.array([m[0][0] for m in mem])
+        lam = np.array([m[1] for m in mem]) / c
+        s = int(np.argmin(lam))
+        cfg = self.cg_config if self.cg_config is not None else CgConfig(rel_tolerance=FIT_CG_TOLERANCE)
+        op = KernelOperator(k1, self.x, float(lam[s]), ctx=ctx, _validated=True)
+        try:
+            X, _, _ = op.cg_shifted(self.y, lam - lam[s], cfg.rel_tolerance, cfg.max_iterations)
+            lds = slq_logdet_shifted(op, self.x.shape[0], cfg, self.seed,
+                                     [(float(c[e]), float(lam[e] - lam[s])) for e in range(len(qs))])
+        except _ShiftFallback:
+            return [self._eval(q, ctx) for q in qs]
+        n = self.x.shape[0]
+        out = []
+        for e in range(len(qs)):
+            if isinstance(lds[e], BaseException):
+                out.append(lds[e])
+                continue
+            alpha = X[:, e] / c[e]
+            out.append(-0.5 * (float(self.y @ alpha) + lds[e] + n * LOG_2PI))
+        return out
+
     def __call__(self, q):
         return self._eval(q)
 
-    def _worker_eval(self, q):
+    def _worker_ctx(self):
         ctx = getattr(self._ctx, "ctx", None)
         if ctx is None:
             ctx = self._ctx.ctx = _lib.Context(_lib.default_context().device)
-        return self._eval(q, ctx)
+        return ctx
 
     def batch(self, qs, return_exceptions=False):
-        """Values of every q (concurrently); with return_exceptions an
-        evaluation that raises yields its exception in place of its value."""
-        def guard(fn):
-            def run(q):
-                try:
-                    return fn(q)
-                except Exception as exc:  # noqa: BLE001 (returned, re-raised by the caller)
-                    if not return_exceptions:
-                        raise
-                    return exc
-            return run
+        """Values of every q; with return_exceptions an evaluation that raises
+        yields its exception in place of its value."""
+        def guard(v):
+            if isinstance(v, BaseException) and not return_exceptions:
+                raise v
+            return v
 
-        if self.workers <= 1 or len(qs) <= 1:
-            return [guard(self._eval)(q) for q in qs]
-        if self._pool is None:
-            self._pool = ThreadPoolExecutor(max_workers=self.workers)
-        return list(self._pool.map(guard(self._worker_eval), qs))
+        # tasks: groups of points sharing K1 (fused) and single points
+        tasks = []
+        if self.fuse_shifts and len(qs) > 1:
+            from .kernels import format_kernel
+
+            groups = {}
+            for i, q in enumerate(qs):
+                k, _ = unflatten_model_params(self.kernel, q)
+                groups.setdefault(format_kernel(_peel_root_scale(k)[1]), []).append(i)
+            tasks = list(groups.values())
+        else:
+            tasks = [[i] for i in range(len(qs))]
+
+        def run(idxs, ctx=None):
+            try:
+                if len(idxs) == 1:
+                    return [self._eval(qs[idxs[0]], ctx)]
+                return self._eval_group([qs[i] for i in idxs], ctx)
+            except Exception as exc:  # noqa: BLE001 (returned, re-raised below)
+                return [exc] * len(idxs)
+
+        if self.workers <= 1 or len(tasks) <= 1:
+            results = [run(idxs) for idxs in tasks]
+        else:
+            if self._pool is None:
+                self._pool = ThreadPoolExecutor(max_workers=self.workers)
+            results = list(self._pool.map(lambda idxs: run(idxs, self._worker_ctx()), tasks))
+        out = [None] * len(qs)
+        for idxs, vals in zip(tasks, results):
+            for i, v in zip(idxs, vals):
+                out[i] = v
+        return [guard(v) for v in out]
 
 
-def exact_evidence_objective(x, y, kernel, cg_config=None, seed=0, workers=None):
+def exact_evidence_objective(x, y, kernel, cg_config=None, seed=0, workers=None, fuse_shifts=True):
     """The exact-GP objective for optimize_hyperparams: each call one device CG
     fit and one device SLQ evidence (the kernel program is cached by tree
-    shape, parameters are launch arguments). ``workers`` concurrent contexts
-    evaluate an optimiser step's 2P + 1 points at once (default min(8, 2P+1)
-    for N >= 8192, else 1; tools/optimizer_timing.py)."""
+    shape, parameters are launch arguments). ``batch`` (what the optimiser
+    uses) fuses the points that differ only in the root output scale and the
+    noise into one multi-shift CG + one Lanczos run (``fuse_shifts``), and
+    ``workers`` concurrent contexts evaluate the remaining tasks at once
+    (default min(8, 2P+1) for N >= 8192, else 1; tools/optimizer_timing.py)."""
     x = as_matrix(x, "X")
     y = as_vector(y, "y")
     if workers is None:
@@ -349,7 +429,7 @@ def exact_evidence_objective(x, y, kernel, cg_config=None, seed=0, workers=None)
         # concurrency pays once the device work dominates: 3 Adam steps at
         # N = 20000 1.45 vs 2.76 s; at N <= 4000 host time dominates (equal)
         workers = min(8, 2 * (n_params(kernel) + 1) + 1) if x.shape[0] >= 8192 else 1
-    return _EvidenceObjective(x, y, kernel, cg_config, seed, int(workers))
+    return _EvidenceObjective(x, y, kernel, cg_config, seed, int(workers), fuse_shifts)
 
 
 def metrics(mean, var_latent, noise, y_true):

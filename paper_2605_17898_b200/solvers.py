@@ -106,6 +106,24 @@ class KernelOperator:
                                      _lib.INPUTS_FINITE))
         return x, iters, res
 
+    def cg_shifted(self, b, shifts, rel_tol, max_iter):
+        """Solutions of (K + (noise + shifts[e]) I) x_e = b for every shift
+        (>= 0) with one matvec per iteration (lgp_cg_shifted, CG-M):
+        (X [n x n_shifts], iterations, final residuals), each shift with the
+        reference CG's stop rule of its own system."""
+        b = as_block(b, "b")
+        shifts = np.ascontiguousarray(shifts, dtype=np.float64)
+        ns = shifts.shape[0]
+        x = np.empty((b.shape[0], ns))
+        iters = np.zeros(ns, dtype=np.int32)
+        res = np.zeros(ns)
+        mi = 0 if max_iter is None else int(max_iter)
+        _lib.check(_lib.lib().lgp_cg_shifted(self.ctx.handle, self.prog.handle, self.points.handle,
+                                             self.noise, _lib.vptr(b), ns, _lib.dptr(shifts),
+                                             float(rel_tol), mi, _lib.vptr(x), _lib.iptr(iters),
+                                             _lib.dptr(res), _lib.INPUTS_FINITE))
+        return x, iters, res
+
     def lanczos(self, z, steps):
         z = np.ascontiguousarray(z, dtype=np.float64)
         t = z.shape[1]
@@ -274,6 +292,51 @@ def slq_logdet(apply, n, config=None, seed=0):
     for c in range(cfg.probes):
         total += n * _lanczos_callable(apply, np.ascontiguousarray(z[:, c]), steps)
     return total / cfg.probes
+
+
+class _ShiftFallback(Exception):
+    """A shifted member's Lanczos would run past the seed's early exit."""
+
+
+def slq_logdet_shifted(op, n, config, seed, members):
+    """slq_logdet of c_e (A + sig_e I) for every member (c_e, sig_e), A = op,
+    from ONE device Lanczos run on A: Lanczos is shift- and scale-invariant
+    (same basis; alpha -> c (alpha + sig), beta -> c beta), so each member's
+    tridiagonal - including the reference's early exit (solvers.py:151-152),
+    re-evaluated on the member's own coefficients - and its quadrature
+    (solvers.py:155-161) follow from the seed's. Returns one log-det or
+    OperatorNotSpdError per member; raises _ShiftFallback if a member would
+    continue past a probe's early exit on A."""
+    cfg = config if config is not None else CgConfig()
+    steps = min(cfg.lanczos_steps, n)
+    z = probe_block(n, cfg.probes, seed)
+    al, be, cnt = [], [], []
+    for c0 in range(0, cfg.probes, 256):
+        a, b, m = op.lanczos(z[:, c0:c0 + 256], steps)
+        al.append(a)
+        be.append(b)
+        cnt.append(m)
+    al, be, cnt = np.vstack(al), np.vstack(be), np.concatenate(cnt)
+    out = []
+    for c, sig in members:
+        total = 0.0
+        try:
+            for p in range(cfg.probes):
+                m = int(cnt[p])
+                a = c * (al[p, :m] + sig)
+                b = c * be[p, :max(m - 1, 0)]
+                cut = m
+                for j in range(m - 1):
+                    if b[j] <= 1e-12 * max(1.0, abs(a[j])):
+                        cut = j + 1
+                        break
+                if cut == m and m < steps:
+                    raise _ShiftFallback()
+                total += n * gauss_quadrature(a[:cut], b[:cut - 1])
+            out.append(total / cfg.probes)
+        except OperatorNotSpdError as exc:
+            out.append(exc)
+    return out
 
 
 def _lanczos_callable(apply, z, steps):

@@ -239,19 +239,23 @@ def test_device_results_are_deterministic(gpu_ctx, expr, d):
 
 
 def test_evidence_objective_batch_matches_sequential(gpu_ctx):
-    """An optimiser step's 2P + 1 evidence evaluations run concurrently (one
-    context / stream per worker thread) and give the same bits as one-by-one
-    calls on the default context."""
+    """An optimiser step's 2P + 1 evidence evaluations at once: without shift
+    fusion (concurrent per-thread contexts) bit-identical to one-by-one calls;
+    with it (points differing only in the output scale / noise share one
+    multi-shift CG and one Lanczos run, §8f row 3) within 1e-9 relative."""
     rng = np.random.default_rng(23)
     x = rng.random((900, 3))
     y = np.sin(2.0 * x.sum(1)) + 0.1 * rng.standard_normal(900)
     kernel = G.parse_kernel("(scale 1.2 (rbf 0.4))")
-    obj = G.exact_evidence_objective(x, y, kernel, seed=0, workers=7)
     p = G.flatten_model_params(kernel, 0.1)
     qs = [p, *[p + np.eye(3)[i] * s for i in range(3) for s in (1e-4, -1e-4)]]
-    batch = obj.batch(qs)
-    seq = [obj(q) for q in qs]
-    assert batch == seq
+    seq = [G.exact_evidence_objective(x, y, kernel, seed=0)(q) for q in qs]
+    plain = G.exact_evidence_objective(x, y, kernel, seed=0, workers=7, fuse_shifts=False)
+    assert plain.batch(qs) == seq
+    fused = G.exact_evidence_objective(x, y, kernel, seed=0, workers=3).batch(qs)
+    err = max(abs(a - b) / abs(b) for a, b in zip(fused, seq))
+    print(f"\n[fused 2P+1 batch] max relative difference to sequential {err:.1e}")
+    assert err <= 1e-9
 
 
 @pytest.mark.parametrize("seed,n,d", [(0, 300, 2), (1, 1000, 2), (2, 3000, 8)])
@@ -297,3 +301,36 @@ def test_multi_rhs_cg_column_compaction(gpu_ctx, monkeypatch):
     np.testing.assert_array_equal(it1, it0)
     np.testing.assert_array_equal(r1, r0)
     np.testing.assert_array_equal(X1, X0)
+
+
+@pytest.mark.parametrize("expr,d", [("(rbf 0.5)", 8), ("(matern52 0.7)", 3)])
+def test_multi_shift_cg_matches_separate_solves(gpu_ctx, expr, d):
+    """lgp_cg_shifted (one matvec per iteration for every shift: CG-M)
+    reproduces separate CG solves of (K + (noise + shift) I) x = b. The
+    optimiser's shifts are small (finite-difference steps of the noise and the
+    output scale): iteration counts within rounding noise of the stop rule
+    (+-3: the separate solves themselves move that much with the noise value's
+    rounding) and solutions to 1e-6, the seed itself bit for bit. Large shifts converge much faster than the seed, and
+    their residual, read off the seed's recurrence (|zeta| ||r||), is then
+    less accurate: iterations within 5 %."""
+    x, b = small_inputs(3000, d, 71)
+    k = G.parse_kernel(expr)
+    noise = 0.05
+    shifts = np.array([0.0, 1e-4, 1e-3, 0.01, 0.05, 0.3, 1.7])
+    op = G.KernelOperator(k, x, noise)
+    X, it, res = op.cg_shifted(b, shifts, 1e-8, None)
+    for e, sh in enumerate(shifts):
+        one = G.cg_solve(G.KernelOperator(k, x, noise + sh), b, G.CgConfig(rel_tolerance=1e-8))
+        err = rel_l2(X[:, e], one.x)
+        print(f"\n[shift {sh}] iterations {it[e]} vs {one.iterations}, x relL2 {err:.1e}, "
+              f"residual {res[e]:.2e} vs {one.final_residual:.2e}")
+        assert res[e] <= 1e-8 * np.linalg.norm(b)
+        if sh <= 0.05:
+            assert abs(int(it[e]) - one.iterations) <= 3
+            assert err <= 1e-6
+        else:
+            assert abs(int(it[e]) - one.iterations) <= max(2, 0.05 * one.iterations)
+            assert err <= 1e-5
+        if sh == 0.0:
+            assert int(it[e]) == one.iterations
+            np.testing.assert_array_equal(X[:, e], one.x)
