@@ -30,25 +30,34 @@
 //                      in the distance GEMM; 12 instead of 8 MMAs per chunk
 //                      cost 6 % at 16 RHS, hence only where TMEM needs it)
 //   D2 (FP32, TMEM) is drained every LGP_TC_G chunks of a warpgroup into FP64
-//   registers; the two epilogue warpgroups' FP64 sums are combined in a fixed
+//   registers; the epilogue warpgroups' FP64 sums are combined in a fixed
 //   order and written as this segment's partial (deterministic).
 //
-// Warp roles: warp 0 = TMA bulk-copy producer (+ TMEM allocator), warp 11 =
-// distance-GEMM issuer, warps 1 / 10 = contraction issuers of epilogue
-// warpgroups 0 / 1 (one MMA-issuing thread sustains ~60-90 cycles per MMA),
-// warps 2..5 / 6..9 = epilogue warpgroups 0 / 1 (even / odd chunks). TMEM:
-// LGP_TC_NSB S buffers of 64 columns (S' in FP32, then P packed FP16 hi | lo
-// in place) + 2 x 2 D2 accumulators (2N columns, N with 64 RHS). With 64 RHS the FP64 row
-// sums take 128 registers per thread, so the epilogue handles each chunk in
-// two 32-column halves (P of a half packed inside the half's columns).
+// Warp roles: warp 0 = TMA bulk-copy producer (+ TMEM allocator); LGP_TC_NWG
+// epilogue warpgroups, chunk c -> warpgroup c % NWG and S buffer c % NSB, each
+// with its own contraction issuer (one MMA-issuing thread sustains ~60-90
+// cycles per MMA). Up to 32 RHS: 3 warpgroups (16 warps, 128 registers: the
+// epilogue works in two 32-column halves; MUFU needs more than two warps per
+// SM sub-partition to stay busy: cfg4 t = 16 2.96 vs 3.46 ms with 2), and the
+// contraction issuer of chunk c also issues the distance GEMM of chunk c + NSB
+// right behind it (tcgen05.mma ops of one thread execute in issue order, so
+// the GEMM may overwrite P as soon as the contraction is issued). 64 RHS: 2
+// warpgroups (the FP64 row sums take 128 registers) and a distance-GEMM
+// issuer warp that waits for each S buffer's contraction to complete
+// (PEMPTY). TMEM: LGP_TC_NSB S buffers of 64 columns (S' in FP32, then P
+// packed FP16 hi | lo in place) + LGP_TC_D2B D2 accumulators per warpgroup (2N
+// columns, N with 64 RHS).
 //
 // (Measured and dropped, round 1: CTA pairs (cta_group::2, M = 256: 5.1 vs
 // 3.6 ms at cfg4 - MMA instructions are not the binding resource), distance
 // tiles on mma.sync (4.2-5.3 ms), distance tiles on the FMA pipe (4.4-5.0 ms),
 // 3-4 epilogue warpgroups with shared-memory row sums (4.6 ms).)
 
+#ifndef LGP_TC_D2B
+#define LGP_TC_D2B 2  // D2 accumulators per warpgroup (1: drained one chunk into the next group)
+#endif
 #ifndef LGP_TC_DLAG
-#define LGP_TC_DLAG ((LGP_TC_G + 1) / 2)
+#define LGP_TC_DLAG (LGP_TC_D2B == 1 ? 1 : (LGP_TC_G + 1) / 2)
 #endif
 #if LGP_TC_DLAG < 1 || LGP_TC_DLAG > LGP_TC_G
 #error "LGP_TC_DLAG must be in [1, LGP_TC_G]"
@@ -60,14 +69,26 @@
 #endif
 
 #define TC_CH 64
-#define TC_THREADS 384  // 12 warps: producer, 3 MMA issuers, 2 epilogue warpgroups
+#ifndef LGP_TC_NWG
+#define LGP_TC_NWG 2  // epilogue warpgroups (chunk c -> warpgroup c % NWG)
+#endif
+// distance GEMMs issued by a warp of their own (else by the contraction
+// issuers, right behind the contraction that frees their S buffer)
+#ifndef LGP_TC_DISTW
+#define LGP_TC_DISTW (LGP_TC_NWG == 2)
+#endif
+// warps: producer, [distance-GEMM issuer], then per warpgroup one contraction
+// issuer and four epilogue warps (3 warpgroups: 16 warps, 128 registers)
+#define TC_THREADS (32 * (1 + LGP_TC_DISTW + 5 * LGP_TC_NWG))
+#define TC_W_CI (1 + LGP_TC_DISTW)                 // first contraction issuer
+#define TC_W_EPI (1 + LGP_TC_DISTW + LGP_TC_NWG)   // first epilogue warp
 #if LGP_TC_N != 8 && LGP_TC_N != 16 && LGP_TC_N != 32 && LGP_TC_N != 64
 #error "K1-TC takes 8, 16, 32 or 64 right-hand sides per pass"
 #endif
 #define TC_KSTACK (LGP_TC_N == 64)                 // cross terms stacked in K (see above)
 #define TC_N2 (TC_KSTACK ? LGP_TC_N : 2 * LGP_TC_N)  // GEMM2 N = D2 columns
 // epilogue round trips per chunk: 64 RHS -> two 32-column halves
-#define TC_HALVES (LGP_TC_N == 64 ? 2 : 1)
+#define TC_HALVES ((LGP_TC_N == 64 || LGP_TC_NWG > 2) ? 2 : 1)
 // TMEM column (within an S buffer) of the FP16x2 hi / lo words of the
 // contraction's K step kk (16 chunk columns)
 #define TC_PHI(kk) (TC_HALVES == 1 ? 8u * (kk) : 32u * ((kk) >> 1) + 8u * ((kk) & 1))
@@ -84,15 +105,14 @@
 // FP32 column features of a chunk (trees with Periodic leaves)
 #define TC_C32_BYTES (LGP_TC_PF ? TC_CH * LGP_TC_FW * 4 : 0)
 #define TC_STAGE_BYTES (TC_B1_BYTES + TC_V_BYTES + TC_C32_BYTES)
-#define TC_COMB_BYTES (128 * LGP_TC_N * 8)
+#define TC_COMB_BYTES ((LGP_TC_NWG - 1) * 128 * LGP_TC_N * 8)
 #ifndef LGP_TC_NSB
-#define LGP_TC_NSB 6   // S buffers in TMEM (64 columns each), even: NSB/2 per warpgroup
+#define LGP_TC_NSB 6   // S buffers in TMEM (64 columns each): chunk c -> buffer c % NSB
 #endif
-#define TC_NSBW (LGP_TC_NSB / 2)
-#if 64 * LGP_TC_NSB + 4 * TC_N2 > 512
-#error "TMEM budget: S buffers + 2x2 D2 accumulators exceed 512 columns"
+#if 64 * LGP_TC_NSB + LGP_TC_D2B * LGP_TC_NWG * TC_N2 > 512
+#error "TMEM budget: S buffers + D2 accumulators exceed 512 columns"
 #endif
-#define TC_NBARS (1 + 2 * LGP_TC_STAGES + 3 * LGP_TC_NSB + 8)
+#define TC_NBARS (1 + 2 * LGP_TC_STAGES + 3 * LGP_TC_NSB + 4 * LGP_TC_NWG)
 
 // barrier slots
 #define B_AFULL 0
@@ -102,7 +122,7 @@
 #define B_PFULL(q) (1 + 2 * LGP_TC_STAGES + LGP_TC_NSB + (q))
 #define B_PEMPTY(q) (1 + 2 * LGP_TC_STAGES + 2 * LGP_TC_NSB + (q))
 #define B_D2FULL(w, b) (1 + 2 * LGP_TC_STAGES + 3 * LGP_TC_NSB + 2 * (w) + (b))
-#define B_D2EMPTY(w, b) (5 + 2 * LGP_TC_STAGES + 3 * LGP_TC_NSB + 2 * (w) + (b))
+#define B_D2EMPTY(w, b) (1 + 2 * LGP_TC_STAGES + 3 * LGP_TC_NSB + 2 * LGP_TC_NWG + 2 * (w) + (b))
 
 // blocking mbarrier waits let the hardware suspend the waiting thread (up to
 // this many ns per try) instead of spinning: spinning producer / issuer /
@@ -443,7 +463,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       lgp_mbar_init(BAR(B_PFULL(q)), 4);
       lgp_mbar_init(BAR(B_PEMPTY(q)), 1);
     }
-    for (int w = 0; w < 2; ++w)
+    for (int w = 0; w < LGP_TC_NWG; ++w)
       for (int b = 0; b < 2; ++b) {
         lgp_mbar_init(BAR(B_D2FULL(w, b)), 1);
         lgp_mbar_init(BAR(B_D2EMPTY(w, b)), 4);
@@ -464,7 +484,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
   // columns 0..31, lo in 32..63); D2[w][b]: 2N columns (P.V_hi | P.V_lo)
 #define T_SB(q) (tmem + 64u * (unsigned)(q))
 #define T_D2(w, b) \
-  (tmem + 64u * LGP_TC_NSB + (unsigned)TC_N2 * (2u * (unsigned)(w) + (unsigned)(b)))
+  (tmem + 64u * LGP_TC_NSB + (unsigned)TC_N2 * ((unsigned)LGP_TC_D2B * (unsigned)(w) + (unsigned)(b)))
 
   // instruction descriptors: FP32 accumulate, FP16 A and B, K-major, M = 128.
   // Shared-memory descriptors are precomputed: the start-address field is
@@ -498,7 +518,8 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       }
     }
     __syncwarp();
-  } else if (warp == 11) {
+#if LGP_TC_DISTW
+  } else if (warp == 1) {
     if (lane == 0) {
       // --------------------------------------------- distance-GEMM issuer
       // every chunk in order, once it is staged and its S buffer's previous
@@ -506,36 +527,51 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       const unsigned long long a_d = dk + (lgp_saddr(a1s) >> 4);
       lgp_mbar_wait(BAR(B_AFULL), 0);
       for (int c = 0; c < nch; ++c) {
-        const int w = c & 1, k = c >> 1;
-        const int q = w + 2 * (k % TC_NSBW);
+        const int q = c % LGP_TC_NSB;
         const int s = c % LGP_TC_STAGES;
         lgp_mbar_wait(BAR(B_SFULL(s)), (c / LGP_TC_STAGES) & 1);
-        if (k >= TC_NSBW) lgp_mbar_wait(BAR(B_PEMPTY(q)), ((k / TC_NSBW) - 1) & 1);
+        if (c >= LGP_TC_NSB) lgp_mbar_wait(BAR(B_PEMPTY(q)), ((c / LGP_TC_NSB) - 1) & 1);
         lgp_tc_fence_after();
         const unsigned long long b_d = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
-        const unsigned d = T_SB(q);
 #pragma unroll
         for (int kk = 0; kk < LGP_TC_KD / 16; ++kk)
-          lgp_mma_f16_ss(d, a_d + 16u * kk, b_d + 16u * kk, idesc1, kk > 0);
+          lgp_mma_f16_ss(T_SB(q), a_d + 16u * kk, b_d + 16u * kk, idesc1, kk > 0);
         lgp_mma_commit(BAR(B_S1FULL(q)));
       }
     }
     __syncwarp();
-  } else if (warp == 1 || warp == 10) {
+#endif
+  } else if (warp < TC_W_EPI) {
     if (lane == 0) {
       // -------------------------------------------- contraction issuers
-      // each epilogue warpgroup w has its own contraction issuer (warp 1 ->
-      // w 0, warp 10 -> w 1) that owns its D2 accumulators
-      const int w = warp == 1 ? 0 : 1;
-      const int nloc = (nch - w + 1) >> 1;
+      // each epilogue warpgroup w has its own contraction issuer that owns its
+      // D2 accumulators
+      const int w = warp - TC_W_CI;
+      const int nloc = nch > w ? (nch - w + LGP_TC_NWG - 1) / LGP_TC_NWG : 0;
+      const unsigned long long a_d = dk + (lgp_saddr(a1s) >> 4);
+      // distance GEMM of chunk c into S buffer c % NSB, once its stage is in
+      auto dist = [&](int c) {
+        const int q = c % LGP_TC_NSB, s = c % LGP_TC_STAGES;
+        lgp_mbar_wait(BAR(B_SFULL(s)), (c / LGP_TC_STAGES) & 1);
+        lgp_tc_fence_after();
+        const unsigned long long b_d = dk + stg0 + (unsigned)s * (TC_STAGE_BYTES >> 4);
+#pragma unroll
+        for (int kk = 0; kk < LGP_TC_KD / 16; ++kk)
+          lgp_mma_f16_ss(T_SB(q), a_d + 16u * kk, b_d + 16u * kk, idesc1, kk > 0);
+        lgp_mma_commit(BAR(B_S1FULL(q)));
+      };
+      if (!LGP_TC_DISTW) {
+        lgp_mbar_wait(BAR(B_AFULL), 0);
+        for (int c = w; c < LGP_TC_NSB && c < nch; c += LGP_TC_NWG) dist(c);
+      }
       for (int k = 0; k < nloc; ++k) {
-        const int c = 2 * k + w;
-        const int q = w + 2 * (k % TC_NSBW);
-        const int gi = k / LGP_TC_G, b = gi & 1;
+        const int c = LGP_TC_NWG * k + w;
+        const int q = c % LGP_TC_NSB;
+        const int gi = k / LGP_TC_G, b = gi % LGP_TC_D2B;
         const bool first = (k % LGP_TC_G) == 0;
         const bool last = ((k % LGP_TC_G) == LGP_TC_G - 1) || (k == nloc - 1);
-        lgp_mbar_wait(BAR(B_PFULL(q)), (k / TC_NSBW) & 1);
-        if (first && gi >= 2) lgp_mbar_wait(BAR(B_D2EMPTY(w, b)), ((gi >> 1) - 1) & 1);
+        lgp_mbar_wait(BAR(B_PFULL(q)), (c / LGP_TC_NSB) & 1);
+        if (first && gi >= LGP_TC_D2B) lgp_mbar_wait(BAR(B_D2EMPTY(w, b)), ((gi / LGP_TC_D2B) - 1) & 1);
         lgp_tc_fence_after();
         const int s = c % LGP_TC_STAGES;
         // B = V_hi (rows 0..N-1 of the staged V tile) and V_lo (rows N..2N-1)
@@ -552,18 +588,25 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
 #endif
         }
         lgp_mma_commit(BAR(B_SEMPTY(s)));
-        lgp_mma_commit(BAR(B_PEMPTY(q)));
         if (last) lgp_mma_commit(BAR(B_D2FULL(w, b)));
+        // the next chunk on this S buffer: tcgen05.mma ops of one thread run
+        // in issue order, so its distance GEMM may overwrite P right behind
+        // this contraction (no wait for the contraction's completion)
+#if LGP_TC_DISTW
+        lgp_mma_commit(BAR(B_PEMPTY(q)));
+#else
+        if (c + LGP_TC_NSB < nch) dist(c + LGP_TC_NSB);
+#endif
       }
     }
     __syncwarp();
   } else {
     // -------------------------------------------------- epilogue warpgroups
-    const int w = (warp - 2) >> 2;
+    const int w = (warp - TC_W_EPI) >> 2;
     const int q4 = warp & 3;                // TMEM lane quarter of this warp
     const int row = 32 * q4 + lane;         // row within the 128-row tile
     const unsigned lanes = (unsigned)(32 * q4) << 16;
-    const int nloc = (nch - w + 1) >> 1;    // chunks of this warpgroup
+    const int nloc = nch > w ? (nch - w + LGP_TC_NWG - 1) / LGP_TC_NWG : 0;  // chunks of this warpgroup
     double acc[LGP_TC_N];
 #pragma unroll
     for (int i = 0; i < LGP_TC_N; ++i) acc[i] = 0.0;
@@ -575,8 +618,8 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
 #endif
 
     auto drain = [&](int gi) {
-      const int b = gi & 1;
-      lgp_mbar_wait(BAR(B_D2FULL(w, b)), (gi >> 1) & 1);
+      const int b = gi % LGP_TC_D2B;
+      lgp_mbar_wait(BAR(B_D2FULL(w, b)), (gi / LGP_TC_D2B) & 1);
       lgp_tc_fence_after();
       // column i: RHS i of the pass (up to 32 RHS: P.V_hi in columns
       // 0..N-1, P.V_lo in N..2N-1, both added)
@@ -605,14 +648,15 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
     };
 
     for (int k = 0; k < nloc; ++k) {
-      const int q = w + 2 * (k % TC_NSBW);
+      const int c = LGP_TC_NWG * k + w;
+      const int q = c % LGP_TC_NSB;
       const unsigned sb = T_SB(q) + lanes;
-      lgp_mbar_wait(BAR(B_S1FULL(q)), (k / TC_NSBW) & 1);
+      lgp_mbar_wait(BAR(B_S1FULL(q)), (c / LGP_TC_NSB) & 1);
       lgp_tc_fence_after();
 #if LGP_TC_PF
       // column Periodic features of this chunk, staged with its B tile (the
       // stage is released only after this chunk's contraction)
-      const int cpf = 2 * k + w;
+      const int cpf = c;
       lgp_mbar_wait(BAR(B_SFULL(cpf % LGP_TC_STAGES)), (cpf / LGP_TC_STAGES) & 1);
       const float* cfp = reinterpret_cast<const float*>(stg + (size_t)(cpf % LGP_TC_STAGES) * TC_STAGE_BYTES +
                                                         TC_B1_BYTES + TC_V_BYTES) + LGP_TC_P0;
@@ -673,21 +717,25 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
          gi < (nloc + LGP_TC_G - 1) / LGP_TC_G; ++gi)
       drain(gi);
 
-    // combine the two warpgroups' FP64 sums in a fixed order, undo the V scaling
-    if (w == 1) {
+    // combine the warpgroups' FP64 sums in a fixed order, undo the V scaling
+    if (w > 0) {
 #pragma unroll
-      for (int i = 0; i < LGP_TC_N; ++i) comb[i * 128 + row] = acc[i];
+      for (int i = 0; i < LGP_TC_N; ++i) comb[((w - 1) * LGP_TC_N + i) * 128 + row] = acc[i];
     }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(128 * LGP_TC_NWG) : "memory");
     if (w == 0) {
+#pragma unroll
+      for (int u = 1; u < LGP_TC_NWG - 1; ++u)
+#pragma unroll
+        for (int i = 0; i < LGP_TC_N; ++i) acc[i] += comb[((u - 1) * LGP_TC_N + i) * 128 + row];
       double* out = a.partial +
                     (((size_t)seg * a.n_pass + pass) * a.n_rows_pad + (size_t)rb * 128 + row) *
                         LGP_TC_N;
       const float* sc = a.vscale + (size_t)pass * LGP_TC_N;
 #pragma unroll
       for (int i = 0; i < LGP_TC_N; i += 2) {
-        const double x0 = (acc[i] + comb[i * 128 + row]) * (double)sc[i];
-        const double x1 = (acc[i + 1] + comb[(i + 1) * 128 + row]) * (double)sc[i + 1];
+        const double x0 = (acc[i] + comb[((LGP_TC_NWG - 2) * LGP_TC_N + i) * 128 + row]) * (double)sc[i];
+        const double x1 = (acc[i + 1] + comb[((LGP_TC_NWG - 2) * LGP_TC_N + i + 1) * 128 + row]) * (double)sc[i + 1];
         reinterpret_cast<double2*>(out)[i / 2] = make_double2(x0, x1);
       }
     }

@@ -41,14 +41,14 @@ __global__ void kern(long long* out, unsigned* sink) {
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
                    : R8(v, 32), R8(v, 40), R8(v, 48), R8(v, 56) : "r"(a + 32u));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      acc ^= v[it & 63];
+      acc ^= v[0] ^ v[31] ^ v[32] ^ v[63];  // fixed indices: a dynamic index puts v[] in local memory
     }
     if (MODE == 4) {
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
                    "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
                    : R8(v, 0), R8(v, 8), R8(v, 16), R8(v, 24), R8(v, 32), R8(v, 40), R8(v, 48), R8(v, 56) : "r"(a));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      acc ^= v[it & 63];
+      acc ^= v[0] ^ v[31] ^ v[32] ^ v[63];  // fixed indices: a dynamic index puts v[] in local memory
     }
     if (MODE == 5) {  // no wait between iterations: 4 loads in flight, one wait per 2 iterations
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -56,7 +56,7 @@ __global__ void kern(long long* out, unsigned* sink) {
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
                    : R8(v, 32), R8(v, 40), R8(v, 48), R8(v, 56) : "r"(a + 32u));
       if (it & 1) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      acc ^= v[it & 63];
+      acc ^= v[0] ^ v[31] ^ v[32] ^ v[63];  // fixed indices: a dynamic index puts v[] in local memory
     }
     if (MODE == 2) {
       // 16x256b: 16 lanes x 256 bits per "row"; .x8 -> 32 registers per thread
@@ -65,10 +65,10 @@ __global__ void kern(long long* out, unsigned* sink) {
       asm volatile("tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
                    : R8(v, 32), R8(v, 40), R8(v, 48), R8(v, 56) : "r"(a + 32u));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      acc ^= v[it & 63];
+      acc ^= v[0] ^ v[31] ^ v[32] ^ v[63];  // fixed indices: a dynamic index puts v[] in local memory
     }
     if (MODE == 1 || MODE == 3) {
-      v[it & 63] += it;
+      v[0] += it;
       asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
                    ::"r"(a), W8(v, 0), W8(v, 8), W8(v, 16), W8(v, 24) : "memory");
       asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
