@@ -448,7 +448,7 @@ def run_ours(args, rank, world):
                                 "§8d: 1 SFU op per RBF entry), MUFU.EX2 at 16/clk/SM",
                     "peak_source": f"{SFU_PER_SM} MUFU.EX2/clk/SM x {SM_COUNT} SMs x {f_mhz:.0f} MHz: "
                                    "tools/alu_bench.cu measures 15.96/clk/SM at ncu "
-                                   "sm__inst_executed_pipe_xu 99.6 %; K1-TC runs that pipe at 61.7 % "
+                                   "sm__inst_executed_pipe_xu 99.6 %; K1-TC runs that pipe at 71.5 % "
                                    "(profiles/r02_k1tc_t16_ncu_summary.txt)",
                     "tensor": {"issued_tflops": tflop, "peak_measured_bf16_tflops": bf16,
                                "frac": tflop / bf16},

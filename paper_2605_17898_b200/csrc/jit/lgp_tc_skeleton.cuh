@@ -79,9 +79,13 @@
 #endif
 // warps: producer, [distance-GEMM issuer], then per warpgroup one contraction
 // issuer and four epilogue warps (3 warpgroups: 16 warps, 128 registers)
-#define TC_THREADS (32 * (1 + LGP_TC_DISTW + 5 * LGP_TC_NWG))
+// contraction issuers: issuer i takes the chunks c = i (mod NCI)
+#ifndef LGP_TC_NCI
+#define LGP_TC_NCI LGP_TC_NWG
+#endif
+#define TC_THREADS (32 * (1 + LGP_TC_DISTW + LGP_TC_NCI + 4 * LGP_TC_NWG))
 #define TC_W_CI (1 + LGP_TC_DISTW)                 // first contraction issuer
-#define TC_W_EPI (1 + LGP_TC_DISTW + LGP_TC_NWG)   // first epilogue warp
+#define TC_W_EPI (1 + LGP_TC_DISTW + LGP_TC_NCI)   // first epilogue warp
 #if LGP_TC_N != 8 && LGP_TC_N != 16 && LGP_TC_N != 32 && LGP_TC_N != 64
 #error "K1-TC takes 8, 16, 32 or 64 right-hand sides per pass"
 #endif
@@ -158,8 +162,8 @@ __device__ __forceinline__ float lgp_ex2x(float x, int px) {
   return px ? lgp_ex2_fma(x) : lgp_ex2(x);
 }
 
-// entries per 16 whose exp2 runs on the FMA pipe instead of MUFU (measured
-// on cfg4: 0 -> 3.86 ms, 2 -> 3.69 ms, 4 -> 3.78 ms)
+// entries per 16 whose exp2 runs on the FMA pipe instead of MUFU (set by the
+// code generator per tree)
 #ifndef LGP_TC_POLY
 #define LGP_TC_POLY 2
 #endif
@@ -546,8 +550,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       // -------------------------------------------- contraction issuers
       // each epilogue warpgroup w has its own contraction issuer that owns its
       // D2 accumulators
-      const int w = warp - TC_W_CI;
-      const int nloc = nch > w ? (nch - w + LGP_TC_NWG - 1) / LGP_TC_NWG : 0;
+      const int ci = warp - TC_W_CI;
       const unsigned long long a_d = dk + (lgp_saddr(a1s) >> 4);
       // distance GEMM of chunk c into S buffer c % NSB, once its stage is in
       auto dist = [&](int c) {
@@ -562,10 +565,12 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       };
       if (!LGP_TC_DISTW) {
         lgp_mbar_wait(BAR(B_AFULL), 0);
-        for (int c = w; c < LGP_TC_NSB && c < nch; c += LGP_TC_NWG) dist(c);
+        for (int c = ci; c < LGP_TC_NSB && c < nch; c += LGP_TC_NCI) dist(c);
       }
-      for (int k = 0; k < nloc; ++k) {
-        const int c = LGP_TC_NWG * k + w;
+      for (int c = ci; c < nch; c += LGP_TC_NCI) {
+        // chunk c: warpgroup w, its k-th chunk (of nloc)
+        const int w = c % LGP_TC_NWG, k = c / LGP_TC_NWG;
+        const int nloc = (nch - w + LGP_TC_NWG - 1) / LGP_TC_NWG;
         const int q = c % LGP_TC_NSB;
         const int gi = k / LGP_TC_G, b = gi % LGP_TC_D2B;
         const bool first = (k % LGP_TC_G) == 0;
