@@ -67,6 +67,34 @@ __global__ void kern(long long* out, unsigned* sink) {
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       acc ^= v[0] ^ v[31] ^ v[32] ^ v[63];  // fixed indices: a dynamic index puts v[] in local memory
     }
+    if (MODE == 8) {  // 16x128b.x16: 32 registers per thread per load
+      asm volatile("tcgen05.ld.sync.aligned.16x128b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : R8(v, 0), R8(v, 8), R8(v, 16), R8(v, 24) : "r"(a));
+      asm volatile("tcgen05.ld.sync.aligned.16x128b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : R8(v, 32), R8(v, 40), R8(v, 48), R8(v, 56) : "r"(a + 32u));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      acc ^= v[0] ^ v[31] ^ v[32] ^ v[63];
+    }
+    if (MODE == 9) {  // 16x64b.x32: 32 registers per thread per load
+      asm volatile("tcgen05.ld.sync.aligned.16x64b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : R8(v, 0), R8(v, 8), R8(v, 16), R8(v, 24) : "r"(a));
+      asm volatile("tcgen05.ld.sync.aligned.16x64b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : R8(v, 32), R8(v, 40), R8(v, 48), R8(v, 56) : "r"(a + 32u));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      acc ^= v[0] ^ v[31] ^ v[32] ^ v[63];
+    }
+    if (MODE == 10) {  // 16x256b.x4 (the symmetric kernel's shape): 16 registers per load, 4 loads
+      asm volatile("tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                   : R8(v, 0), R8(v, 8) : "r"(a));
+      asm volatile("tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                   : R8(v, 16), R8(v, 24) : "r"(a + 16u));
+      asm volatile("tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                   : R8(v, 32), R8(v, 40) : "r"(a + 32u));
+      asm volatile("tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                   : R8(v, 48), R8(v, 56) : "r"(a + 48u));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      acc ^= v[0] ^ v[31] ^ v[32] ^ v[63];
+    }
     if (MODE == 1 || MODE == 3) {
       v[0] += it;
       asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
@@ -160,6 +188,9 @@ int main(int argc, char** argv) {
     if (mode == 5) run<5>("ld x32 x2, wait every 2nd", w);
     if (mode == 6 && w <= 8) run_two(w);
     if (mode == 7 && w == 4) run_total();
+    if (mode == 8 && w <= 8) run<8>("ld 16x128b.x16 x2", w);
+    if (mode == 9 && w <= 8) run<9>("ld 16x64b.x32 x2", w);
+    if (mode == 10 && w <= 8) run<10>("ld 16x256b.x4 x4", w);
   }
   return 0;
 }
