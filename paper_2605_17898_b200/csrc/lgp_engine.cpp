@@ -737,17 +737,52 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   // single RHS on the symmetric tensor-core kernel: the fused iteration (4
   // launches: pack+p-update, K1, records+p.Ap+step, x/r update+r.r+beta)
   const bool fused = op.tcsym && t == 1 && !std::getenv("LGP_CG_UNFUSED");
-  double* part1 = nullptr;
+  // one rank: the whole vector step is one cooperative launch (cg1_vec), the
+  // next direction and K1 operand included (LGP_CG_VEC3=1: the 3-launch form)
+  const bool vec1 = fused && !split && !std::getenv("LGP_CG_VEC3");
+  const int64_t n_pack = std::max(op.n_rows_pad, op.n_cols_pad);
+  double *part1 = nullptr, *part2 = nullptr;
   unsigned* cnt1 = nullptr;
   if (fused) {
     const size_t np = (size_t)std::max<int64_t>(op.n_tiles, vec::cg1_blocks(n));
-    part1 = (double*)ctx->scratch_get("cg.part1", np * 8 + 16);
-    cnt1 = reinterpret_cast<unsigned*>(part1 + np);
-    LGP_CUDA_CHECK(cudaMemsetAsync(cnt1, 0, 16, ctx->stream));
+    const size_t ncnt = 4;  // the 3-launch form's ticket, or cg1_vec's barrier
+    part1 = (double*)ctx->scratch_get("cg.part1", 2 * np * 8 + ncnt * 4);
+    part2 = part1 + np;
+    cnt1 = reinterpret_cast<unsigned*>(part1 + 2 * np);
+    LGP_CUDA_CHECK(cudaMemsetAsync(cnt1, 0, ncnt * 4, ctx->stream));
+    if (vec1) vec::cg1_pack(ctx, b.p, b.r, op.vpack, n, n_pack, b.s);  // beta = 0: p = r = b
+  }
+  unsigned long long* vtrace = nullptr;
+  if (vec1 && std::getenv("LGP_CG_VEC_TRACE")) {
+    vtrace = (unsigned long long*)ctx->scratch_get("cg.vtrace", (size_t)ctx->sm_count * 8 * 8);
+    LGP_CUDA_CHECK(cudaMemsetAsync(vtrace, 0, (size_t)ctx->sm_count * 8 * 8, ctx->stream));
   }
   for (int it = 1; it <= max_iter && !done_h; ++it) {
-    if (fused) {
-      vec::cg1_pack(ctx, b.p, b.r, op.vpack, n, std::max(op.n_rows_pad, op.n_cols_pad), b.s);
+    if (vec1) {
+      {
+        auto ev = k1_event_begin(ctx);
+        op.tcsym_kernel(b.s.done);
+        k1_event_end(ctx, ev);
+      }
+      vec::cg1_vec(ctx, op.partial, op.colpart, op.r_ptr, op.r_rec, op.c_ptr, op.c_rec, n, n_pack,
+                   op.plan.root_scale, noise, b.x, b.r, b.p, b.ap, op.vpack, part1, part2, cnt1, it,
+                   max_iter, b.s, vtrace);
+      if (vtrace != nullptr && it == 3) {
+        // diagnostics: phase boundaries of the third vector step, CTA 0 and
+        // the latest CTA, microseconds from CTA 0's start
+        std::vector<unsigned long long> tr((size_t)ctx->sm_count * 8);
+        LGP_CUDA_CHECK(cudaMemcpyAsync(tr.data(), vtrace, tr.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        LGP_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        for (int k = 0; k < 8; ++k) {
+          unsigned long long mx = 0;
+          for (int bk = 0; bk < ctx->sm_count; ++bk) mx = std::max(mx, tr[(size_t)bk * 8 + k]);
+          std::fprintf(stderr, "cg1_vec phase %d: cta0 %.2f us, max %.2f us\n", k, (tr[k] - tr[0]) * 1e-3,
+                       (mx - tr[0]) * 1e-3);
+        }
+      }
+      if (nsh > 0) vec::cg_shift(ctx, xs, ps, b.r, n, nsh, sig, sst, b.s, it);
+    } else if (fused) {
+      vec::cg1_pack(ctx, b.p, b.r, op.vpack, n, n_pack, b.s);
       {
         auto ev = k1_event_begin(ctx);
         op.tcsym_kernel(b.s.done);

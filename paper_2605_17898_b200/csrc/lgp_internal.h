@@ -394,6 +394,14 @@ void tcsym_epilogue_cg(Context* c, const double* rowpart, const double* colpart,
                        double scale, double noise, const double* p, double* out, double* part,
                        unsigned* counter, CgState s);
 int cg1_blocks(int64_t n);
+// the whole single-RHS CG vector step in one cooperative launch (records ->
+// Ap, p.Ap, step, x / r update, r.r, beta / convergence, p and the K1
+// operand); bar: 2 unsigned, zeroed once
+void cg1_vec(Context* c, const double* rowpart, const double* colpart, const int* r_ptr,
+             const int* r_rec, const int* c_ptr, const int* c_rec, int64_t n, int64_t n_pad, double scale,
+             double noise, double* x, double* r, double* p, double* ap, double* vpack, double* part_pap,
+             double* part_rs, unsigned* bar, int it, int max_iter, CgState s,
+             unsigned long long* trace = nullptr);
 // dst[i][k] = src[i][map[k]] for k < t_run (src n x t) / dst[i][map[k]] = src[i][k]
 void gather_cols(Context* c, const double* src, int64_t n, int t, const int* map, int t_run,
                  double* dst, const int* done);

@@ -57,6 +57,32 @@ __device__ __forceinline__ double sum_records(const double* __restrict__ data, c
 }
 
 
+// sum_records for the column pair (jj, jj + 1) with 16-byte loads: the same
+// records in the same order per column (bit-identical), up to 4 x 16 bytes in
+// flight per round whatever the record count
+template <int width>
+__device__ __forceinline__ double2 sum_records2(const double* __restrict__ data, const int* __restrict__ rec,
+                                                int e0, int e1, int g, int jj) {
+  double sx = 0.0, sy = 0.0;
+  for (int e = e0 + g; e < e1; e += 4 * kTsGroups) {
+    int r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = e + u * kTsGroups < e1 ? __ldg(rec + e + u * kTsGroups) : -1;
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = r[u] >= 0 ? *reinterpret_cast<const double2*>(data + (size_t)r[u] * width + jj)
+                       : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (r[u] >= 0) {
+        sx += v[u].x;
+        sy += v[u].y;
+      }
+  }
+  return make_double2(sx, sy);
+}
+
 // block partial of sum_i a[i][c]*b[i][c] over this block's row range -> part[blk][c]
 __device__ __forceinline__ void block_colsum(double v, int t, double* part_row, double* sm) {
   const int tid = threadIdx.x;
@@ -442,15 +468,22 @@ __device__ bool deposit_last(double val, double* part, unsigned* counter, int nb
 __device__ double sum_shares(const double* part, int nblk, double* sm) {
   double v = 0.0;
   if (threadIdx.x < 64) {
-    // 8 loads in flight per round (in-order issue would otherwise wait out
+    // 16 loads in flight per round (in-order issue would otherwise wait out
     // one L2 round trip per share); the adds keep the index order
     int b = threadIdx.x;
-    for (; b + 7 * 64 < nblk; b += 8 * 64) {
-      double x[8];
+    for (; b + 15 * 64 < nblk; b += 16 * 64) {
+      double x[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldcg(part + b + 64 * u);
+      for (int u = 0; u < 16; ++u) x[u] = __ldcg(part + b + 64 * u);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v += x[u];
+      for (int u = 0; u < 16; ++u) v += x[u];
+    }
+    for (; b + 3 * 64 < nblk; b += 4 * 64) {
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __ldcg(part + b + 64 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v += x[u];
     }
     for (; b < nblk; b += 64) v += __ldcg(part + b);
   }
@@ -570,6 +603,207 @@ __global__ void __launch_bounds__(256) k_cg1_update(double* __restrict__ x, doub
       *counter = 0u;
     }
   }
+}
+
+// ------------------------------------------ one-launch CG vector step
+// Everything of a single-RHS CG iteration except the matvec, as ONE
+// cooperative launch (one CTA of 1024 threads per SM, co-resident): records
+// -> Ap (+ noise p) and the p.Ap shares | grid barrier | step, x += step p,
+// r -= step Ap and the r.r shares | grid barrier | beta / convergence, p =
+// beta p + r and the K1 operand. Every CTA sums the shares itself (same fixed
+// 64-lane order as sum_shares), so no CTA waits for a "last block", and the
+// arithmetic is the 3-kernel sequence's bit for bit: the p.Ap shares are
+// per 64-row block (k_tcsym_epilogue_cg / k_cg1_pap), the r.r shares per
+// virtual 256-thread block of k_cg1_update's grid-stride layout.
+constexpr int kVecThreads = 1024;
+constexpr int kVecQB = kVecThreads / 256;  // 64-row blocks per record round
+
+// generation barrier over the co-resident grid: bar[0] arrivals, bar[1]
+// generation (a flag per CTA polled by every CTA measured 10 us, this 2 us)
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1u) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// sum_shares with the shares staged through shared memory by the whole CTA
+// (one L2 round trip for up to `cap` shares instead of one per 16 per lane):
+// lane L still adds the shares b = L (mod 64) in index order (cap % 64 == 0)
+__device__ double sum_shares_staged(const double* part, int nblk, double* stg, int cap, double* sm) {
+  double v = 0.0;
+  for (int base = 0; base < nblk; base += cap) {
+    const int m = min(cap, nblk - base);
+    for (int k = threadIdx.x; k < m; k += blockDim.x) stg[k] = __ldcg(part + base + k);
+    __syncthreads();
+    if (threadIdx.x < 64)
+      for (int k = threadIdx.x; k < m; k += 64) v += stg[k];
+    __syncthreads();
+  }
+  return block_sum_fixed(v, sm);
+}
+
+__global__ void __launch_bounds__(kVecThreads, 1)
+    k_cg1_vec(const double* __restrict__ rowpart, const double* __restrict__ colpart,
+              const int* __restrict__ r_ptr, const int* __restrict__ r_rec, const int* __restrict__ c_ptr,
+              const int* __restrict__ c_rec, long long n, long long n_pad, double scale, double noise,
+              double* x, double* r, double* p, double* ap, double* vpack, double* part_pap,
+              double* part_rs, int nvb, unsigned* bar, int it, int max_iter, CgState s,
+              unsigned long long* trace) {
+  // trace (diagnostics, LGP_CG_VEC_TRACE): %globaltimer at the phase
+  // boundaries, per CTA
+  auto stamp = [&](int k) {
+    if (trace != nullptr && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[(size_t)blockIdx.x * 8 + k] = t;
+    }
+  };
+  stamp(0);
+  __shared__ double pt[kVecQB][2][kTsGroups][64];
+  __shared__ double sm[32];
+  __shared__ double ws[32];
+  if (*s.done) return;  // written only by earlier launches: the same for every CTA
+  const double rs_old = s.rs[0];
+  const long long nc = (n + 63) / 64;
+  {
+    // ---- records -> Ap, p.Ap share of each 64-row block: kVecQB blocks per
+    // round, 256 threads each = 8 record groups x 32 column pairs (measured:
+    // 128 threads x 4 columns 10.1 us, both lists' loads interleaved 9.1 us,
+    // this 8.6 us at cfg4: the record reads are throughput-, not latency-bound)
+    const int qb = threadIdx.x >> 8, lt = threadIdx.x & 255;
+    const int j2 = 2 * (lt & 31), g = lt >> 5;
+    // record-list bounds of this thread's block, one round ahead (the
+    // bounds -> indices -> records chain is three dependent L2 round trips)
+    auto bounds = [&](long long c, int4& e) {
+      if (c < nc) {
+        const int I = (int)(c >> 1);
+        e = make_int4(__ldg(c_ptr + c), __ldg(c_ptr + c + 1), __ldg(r_ptr + I), __ldg(r_ptr + I + 1));
+      }
+    };
+    int4 eb = make_int4(0, 0, 0, 0), en = eb;
+    bounds((long long)kVecQB * blockIdx.x + qb, eb);
+    for (long long c0 = (long long)kVecQB * blockIdx.x; c0 < nc; c0 += (long long)kVecQB * gridDim.x) {
+      const long long c = c0 + qb;
+      bounds(c + (long long)kVecQB * gridDim.x, en);
+      // this block's p entries, loaded alongside the records
+      const double pi = (lt < 64 && c < nc && c * 64 + lt < n) ? p[c * 64 + lt] : 0.0;
+      if (c < nc) {
+        const int rr = (int)(c & 1) * 64 + j2;
+        const double2 cs = sum_records2<64>(colpart, c_rec, eb.x, eb.y, g, j2);
+        const double2 rs = sum_records2<128>(rowpart, r_rec, eb.z, eb.w, g, rr);
+        pt[qb][0][g][j2] = cs.x;
+        pt[qb][0][g][j2 + 1] = cs.y;
+        pt[qb][1][g][j2] = rs.x;
+        pt[qb][1][g][j2 + 1] = rs.y;
+      }
+      __syncthreads();
+      if (lt < 64) {
+        const int jj = lt;
+        const long long i = c * 64 + jj;
+        double d = 0.0;
+        if (c < nc && i < n) {
+          double o = 0.0;
+#pragma unroll
+          for (int u = 0; u < kTsGroups; ++u) o += pt[qb][0][u][jj];
+#pragma unroll
+          for (int u = 0; u < kTsGroups; ++u) o += pt[qb][1][u][jj];
+          o = __dmul_rn(scale, o);
+          if (noise != 0.0) o = __dadd_rn(o, __dmul_rn(noise, pi));
+          ap[i] = o;
+          d = pi * o;
+        }
+        // block_sum_fixed of the 64-thread block: each warp's xor tree, then
+        // the two warps in order
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if ((lt & 31) == 0) ws[2 * qb + (lt >> 5)] = d;
+      }
+      __syncthreads();
+      if (c < nc && lt == 0) part_pap[c] = (0.0 + ws[2 * qb]) + ws[2 * qb + 1];
+      eb = en;
+    }
+  }
+  stamp(1);
+  grid_sync(bar);
+  stamp(2);
+  double* stg = &pt[0][0][0][0];  // the record buffers are free now
+  const double pap = sum_shares_staged(part_pap, (int)nc, stg, kVecQB * 2 * kTsGroups * 64, sm);
+  stamp(3);
+  const double st = rs_old / pap;
+  if (pap <= 0.0) {  // breakdown: operator not SPD (solvers.py:110-113)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && s.active[0]) {
+      *s.status = 1;
+      *s.bad_col = 0;
+      *s.done = 1;
+      s.step[0] = st;
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.step[0] = st;
+  // ---- x, r update and the r.r share of each virtual block (k_cg1_update)
+  const int vb = blockIdx.x * (kVecThreads / 256) + (threadIdx.x >> 8);
+  const long long stride = (long long)nvb * 256;
+  double acc = 0.0;
+  if (vb < nvb) {
+    for (long long i = (long long)vb * 256 + (threadIdx.x & 255); i < n; i += stride) {
+      x[i] = __dadd_rn(x[i], __dmul_rn(st, p[i]));
+      const double rv = __dsub_rn(r[i], __dmul_rn(st, __ldcg(ap + i)));  // ap: other CTAs' stores
+      r[i] = rv;
+      acc = fma(rv, rv, acc);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __syncthreads();  // ws reuse
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (vb < nvb && (threadIdx.x & 255) == 0) {
+    double t = 0.0;
+    const int w0 = threadIdx.x >> 5;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += ws[w0 + w];
+    part_rs[vb] = t;
+  }
+  stamp(4);
+  grid_sync(bar);
+  stamp(5);
+  const double rs_new = sum_shares_staged(part_rs, nvb, stg, kVecQB * 2 * kTsGroups * 64, sm);
+  stamp(6);
+  const double nrm = sqrt(rs_new);
+  if (nrm <= s.tol[0] || it >= max_iter) {  // converged, or budget spent (reported)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      s.iters[0] = it;
+      s.res[0] = nrm;
+      s.active[0] = 0;
+      *s.done = 1;
+    }
+    return;
+  }
+  const double beta = rs_new / rs_old;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s.beta[0] = beta;
+    s.rs[0] = rs_new;
+  }
+  // ---- p = beta p + r (the next iteration's direction) and the K1 operand
+  if (vb < nvb) {
+    for (long long i = (long long)vb * 256 + (threadIdx.x & 255); i < n; i += stride) {
+      const double v = __dadd_rn(__dmul_rn(p[i], beta), r[i]);
+      p[i] = v;
+      vpack[i] = v;
+    }
+  }
+  stamp(7);
 }
 
 // ------------------------------------------------ multi-shift CG (CG-M)
@@ -1238,6 +1472,25 @@ void tcsym_epilogue_cg(Context* c, const double* rowpart, const double* colpart,
   k_tcsym_epilogue_cg<<<(unsigned)((n + 63) / 64), 64 * kTsGroups, 0, c->stream>>>(
       rowpart, colpart, r_ptr, r_rec, c_ptr, c_rec, n, scale, noise, p, out, part, counter, s);
   LGP_LAUNCH_CHECK(c);
+}
+
+void cg1_vec(Context* c, const double* rowpart, const double* colpart, const int* r_ptr,
+             const int* r_rec, const int* c_ptr, const int* c_rec, int64_t n, int64_t n_pad, double scale,
+             double noise, double* x, double* r, double* p, double* ap, double* vpack, double* part_pap,
+             double* part_rs, unsigned* bar, int it, int max_iter, CgState s,
+             unsigned long long* trace) {
+  if (n <= 0) return;
+  int nvb = cg1_blocks(n);
+  long long n_ll = n, npad_ll = n_pad;
+  void* args[] = {(void*)&rowpart, (void*)&colpart, (void*)&r_ptr, (void*)&r_rec, (void*)&c_ptr,
+                  (void*)&c_rec, (void*)&n_ll, (void*)&npad_ll, (void*)&scale, (void*)&noise,
+                  (void*)&x, (void*)&r, (void*)&p, (void*)&ap, (void*)&vpack, (void*)&part_pap,
+                  (void*)&part_rs, (void*)&nvb, (void*)&bar, (void*)&it, (void*)&max_iter, (void*)&s,
+                  (void*)&trace};
+  // one CTA per SM, and enough virtual 256-thread blocks per CTA
+  const int grid = std::max(c->sm_count, (nvb + kVecThreads / 256 - 1) / (kVecThreads / 256));
+  LGP_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_cg1_vec, dim3((unsigned)grid),
+                                             dim3(kVecThreads), args, 0, c->stream));
 }
 
 int cg1_blocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (n + 255) / 256)); }

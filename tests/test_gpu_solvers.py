@@ -334,3 +334,20 @@ def test_multi_shift_cg_matches_separate_solves(gpu_ctx, expr, d):
         if sh == 0.0:
             assert int(it[e]) == one.iterations
             np.testing.assert_array_equal(X[:, e], one.x)
+
+
+@pytest.mark.parametrize("expr,d,n,noise", [("(scale 1.3 (rbf 0.5))", 8, 9000, 0.1),
+                                            ("(+ (scale 1.0 (rbf 0.5)) (scale 0.5 (periodic 1.0 0.8)))", 2, 7000, 0.05)])
+def test_one_launch_cg_vector_step_is_bit_identical(gpu_ctx, monkeypatch, expr, d, n, noise):
+    """The cooperative one-launch vector step (k_cg1_vec) reproduces the
+    three-kernel step (records + p.Ap + step | x/r update + r.r + beta | next
+    direction) bit for bit: same shares, same fixed summation orders."""
+    rng = np.random.default_rng(11)
+    x, b = rng.random((n, d)), rng.standard_normal(n)
+    op = G.KernelOperator(G.parse_kernel(expr), x, noise)
+    x1, it1, r1 = op.cg(b, 1e-9, None)
+    x1, it1, r1 = x1.copy(), int(it1[0]), float(r1[0])
+    monkeypatch.setenv("LGP_CG_VEC3", "1")
+    x3, it3, r3 = op.cg(b, 1e-9, None)
+    assert it1 == int(it3[0]) and r1 == float(r3[0])
+    np.testing.assert_array_equal(x1, x3)
