@@ -18,6 +18,8 @@ _lib.check(lib.lgp_host_alloc(x.nbytes, C.byref(hx)))
 _lib.check(lib.lgp_host_alloc(z.nbytes, C.byref(hv)))
 px = np.ctypeslib.as_array(C.cast(hx, C.POINTER(C.c_double)), shape=x.shape); px[...] = x
 pv = np.ctypeslib.as_array(C.cast(hv, C.POINTER(C.c_double)), shape=z.shape); pv[...] = z
+if "--pageable" in sys.argv:  # ordinary NumPy arrays, as the bench's e2e leg passes them
+    px, pv = x.copy(), z.copy()
 for _ in range(12):
     res = G.matrix_free_matvec(k, px, 0.1, pv)
 T = {}
