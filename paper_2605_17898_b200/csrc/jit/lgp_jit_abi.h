@@ -74,7 +74,8 @@ struct LgpTcArgs {
   int n_pass;
   int tiles_per_seg;
   int n_tiles;
-  int pad_[2];
+  int seg_base;         // first column segment of this launch (staged uploads: one launch per part)
+  int pad_;
   float kc[LGP_MAX_KC];
 };
 

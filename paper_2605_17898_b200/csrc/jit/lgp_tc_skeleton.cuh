@@ -436,7 +436,7 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
   if (a.done != nullptr && *a.done) return;
   const int rb = blockIdx.x % a.n_rb;
   const int rest = blockIdx.x / a.n_rb;
-  const int seg = rest % a.n_seg;
+  const int seg = a.seg_base + rest % a.n_seg;  // n_seg: the segments of this launch
   const int pass = rest / a.n_seg;
   const int tile0 = seg * a.tiles_per_seg;
   int nch = a.n_tiles - tile0;

@@ -210,6 +210,9 @@ int lgp_ctx_destroy(lgp_ctx* ctx) {
     if (kv.second->mod) drv::ModuleUnload(kv.second->mod);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
   if (ctx->done_pin) cudaFreeHost(ctx->done_pin);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (cudaEvent_t e : ctx->copy_ev)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->done_ev)
     if (e) cudaEventDestroy(e);
   for (auto& kv : ctx->pool)
@@ -496,14 +499,12 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
   lgp_partition(n, ctx->world, ctx->rank, &r0, &r1);
   const int64_t S = (n + ctx->world - 1) / ctx->world;
   const int64_t n_alloc = S * ctx->world;
-  const double* Vd = stage_in(ctx, "api.V", V, cols->n, t, cols->n, flags);
-  // validate V on the host while its copy is in flight (pinned V: the DMA and
-  // the scan overlap); a non-finite V throws before any kernel is launched
-  if (!(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE))) check_finite(V, (size_t)cols->n * t, "V");
+  const bool scan_v = !(flags & (LGP_DEVICE_PTRS | LGP_INPUTS_FINITE));
   double* od = (flags & LGP_DEVICE_PTRS) && !ctx->sharded()
                    ? out
                    : (double*)ctx->scratch_get("api.out", (size_t)n_alloc * t * 8);
   if (cols->n == 0) {
+    if (scan_v) check_finite(V, (size_t)cols->n * t, "V");
     LGP_CUDA_CHECK(cudaMemsetAsync(od, 0, (size_t)n * t * 8, ctx->stream));
   } else {
     MatvecOp op;
@@ -518,7 +519,22 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
     op.allow_tc = true;
     op.tag = "api.mv";
     op.prepare();
-    op.run(Vd, od + r0 * t, square ? noise : 0.0, square ? Vd + r0 * t : nullptr, nullptr);
+    // host V on one GPU through the tensor-core kernel: the upload in two
+    // parts, the second overlapping the first part's K1 (MatvecOp::run_staged)
+    bool staged = false;
+    if (!(flags & LGP_DEVICE_PTRS) && !ctx->sharded() && !std::getenv("LGP_NO_STAGED")) {
+      double* vd = (double*)ctx->scratch_get("api.V", (size_t)cols->n * t * 8);
+      staged = op.run_staged(V, vd, od, square ? noise : 0.0, square, [&]() {
+        if (scan_v) check_finite(V, (size_t)cols->n * t, "V");  // while part 0 is in flight
+      });
+    }
+    if (!staged) {
+      const double* Vd = stage_in(ctx, "api.V", V, cols->n, t, cols->n, flags);
+      // validate V on the host while its copy is in flight (pinned V: the DMA
+      // and the scan overlap); a non-finite V throws before any kernel is launched
+      if (scan_v) check_finite(V, (size_t)cols->n * t, "V");
+      op.run(Vd, od + r0 * t, square ? noise : 0.0, square ? Vd + r0 * t : nullptr, nullptr);
+    }
     if (ctx->sharded()) comm_allgather_inplace(ctx->comm, od, (size_t)S * t, ctx->stream);
   }
   stage_out(ctx, out, od, (size_t)n * t * 8, flags);

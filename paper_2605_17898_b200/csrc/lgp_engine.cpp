@@ -479,6 +479,75 @@ void MatvecOp::tcsym_kernel(const int* done) {
            plan.smem_tcsym_fixed + (size_t)4096 * ts_R, &a);
 }
 
+bool MatvecOp::run_staged(const double* V_host, double* V_dev, double* out_dev, double noise,
+                          bool square, const std::function<void()>& after_copy0) {
+  if (!plan.tc || tcsym || n_pass != 1 || n_seg < 2) return false;
+  const int tb = plan.tune.tb;
+  if (!ctx->copy_stream) {
+    LGP_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : ctx->copy_ev) LGP_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // V_dev is context scratch: earlier work on the main stream may still read it
+  LGP_CUDA_CHECK(cudaEventRecord(ctx->copy_ev[1], ctx->stream));
+  LGP_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[1], 0));
+  // parts = runs of consecutive column segments (the K1 launch order runs
+  // segment by segment)
+  int parts = 2;
+  if (const char* e = std::getenv("LGP_STAGED_PARTS")) parts = std::max(1, atoi(e));
+  parts = std::min(parts, n_seg);
+  const int seg_per = (n_seg + parts - 1) / parts;
+  const int64_t ncols = cols->n;
+  LgpTcArgs a = plan.tca;
+  a.v_inexact = v_inexact;
+  a.vscale = vscale;
+  a.a1 = fr;
+  a.b1 = fc;
+  a.r32 = r32;
+  a.c32 = c32;
+  a.v = vtc;
+  a.partial = partial;
+  a.done = nullptr;
+  a.n_rows_pad = n_rows_pad;
+  a.n_rb = n_rb;
+  a.n_pass = n_pass;
+  a.tiles_per_seg = tiles_per_seg;
+  a.n_tiles = n_tiles;
+  for (int h = 0; h * seg_per < n_seg; ++h) {
+    const int s0 = h * seg_per, s1 = std::min(n_seg, s0 + seg_per);
+    const int64_t r0 = std::min<int64_t>((int64_t)s0 * tiles_per_seg * 64, ncols);
+    const int64_t r1 = std::min<int64_t>((int64_t)s1 * tiles_per_seg * 64, ncols);
+    if (r1 <= r0 || s1 <= s0) continue;
+    LGP_CUDA_CHECK(cudaMemcpyAsync(V_dev + r0 * t, V_host + r0 * t, (size_t)(r1 - r0) * t * 8,
+                                   cudaMemcpyHostToDevice, ctx->copy_stream));
+    LGP_CUDA_CHECK(cudaEventRecord(ctx->copy_ev[h & 1], ctx->copy_stream));
+    if (h == 0 && after_copy0) {
+      try {
+        after_copy0();
+      } catch (...) {
+        cudaStreamSynchronize(ctx->copy_stream);  // the caller may free V right away
+        throw;
+      }
+    }
+    LGP_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->copy_ev[h & 1], 0));
+    // per-part power-of-two column scales: the K1 undoes them per CTA, and a
+    // power-of-two change only shifts the FP16 exponents
+    const int tile0 = s0 * tiles_per_seg;
+    vec::pack_rhs_tc(ctx, V_dev + r0 * t, r1 - r0, t, (int)ceil_div<int64_t>(r1 - r0, 64), tb, 1,
+                     static_cast<char*>(vtc) + (size_t)tile0 * 2 * tb * 64 * 2, vscale, v_inexact,
+                     nullptr);
+    a.seg_base = s0;
+    a.n_seg = s1 - s0;
+    const int64_t grid = (int64_t)n_rb * (s1 - s0) * n_pass;
+    if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
+    auto ev = k1_event_begin(ctx);
+    launch(ctx, mod->matvec, (unsigned)grid, 1, plan.tune.threads, plan.smem_bytes, &a);
+    k1_event_end(ctx, ev);
+  }
+  vec::epilogue(ctx, partial, n_seg, n_pass, n_rows_pad, tb, n_rows, t, plan.root_scale, noise,
+                square ? V_dev + row0 * t : nullptr, out_dev, nullptr);
+  return true;
+}
+
 void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const double* noise_v,
                    const int* done) {
   const int tb = plan.tune.tb;
@@ -513,6 +582,7 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     a.n_pass = n_pass;
     a.tiles_per_seg = tiles_per_seg;
     a.n_tiles = n_tiles;
+    a.seg_base = 0;
     const int64_t grid = (int64_t)n_rb * n_seg * n_pass;
     if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
     prof_begin();

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -179,6 +180,8 @@ struct Context {
   uint64_t launches = 0;
   void* flush_buf = nullptr;
   int* done_pin = nullptr;               // pinned ring of device done-flag copies (solver loops)
+  cudaStream_t copy_stream = nullptr;    // staged host->device uploads (MatvecOp::run_staged)
+  cudaEvent_t copy_ev[2] = {};
   cudaEvent_t done_ev[16] = {};          // ... and their completion events
   size_t flush_bytes = 0;
   // K1 timing (lgp_ctx_set_profile): event pairs around every fused-matvec
@@ -280,6 +283,14 @@ struct MatvecOp {
   void prepare();  // features, scratch, schedule
   void run(const double* V_dev, double* out_dev, double noise, const double* noise_v,
            const int* done);
+  // K1-TC with V in (pageable or pinned) host memory: V's upload in two parts
+  // on the copy stream, each part's pack + K1 launch (its column segments)
+  // queued as soon as the part has landed, so the second part's transfer
+  // overlaps the first part's K1. True if it ran (else the caller stages V).
+  // after_copy0 runs on the host once the first part's copy is queued (the
+  // host-side V scan); if it throws, nothing has been launched on V yet.
+  bool run_staged(const double* V_host, double* V_dev, double* out_dev, double noise, bool square,
+                  const std::function<void()>& after_copy0);
   // K1-TC-sym alone, on the already packed vpack (fused CG iteration)
   void tcsym_kernel(const int* done);
 };

@@ -402,3 +402,17 @@ def test_deferred_validation_large_inputs(gpu_ctx):
         G.matrix_free_matvec(k, x, -1.0, bad_v)
     good = G.matrix_free_matvec(k, x, 0.1, v)
     assert np.isfinite(good).all()
+
+
+def test_staged_host_upload_matches_one_copy(gpu_ctx, monkeypatch):
+    """Host V through the tensor-core kernel is uploaded in two parts, the
+    second overlapping the first part's K1 (MatvecOp::run_staged, per-part
+    power-of-two column scales): bit-identical to the one-copy path."""
+    rng = np.random.default_rng(17)
+    x = rng.random((50000, 8))
+    v = rng.standard_normal((50000, 16))
+    k = G.parse_kernel("(scale 1.3 (rbf 0.5))")
+    a = G.matrix_free_matvec(k, x, 0.1, v)
+    monkeypatch.setenv("LGP_NO_STAGED", "1")
+    b = G.matrix_free_matvec(k, x, 0.1, v)
+    np.testing.assert_array_equal(a, b)
