@@ -344,10 +344,14 @@ def test_results_in_pinned_buffers_survive(gpu_ctx):
 
 
 @pytest.mark.parametrize("env", [{"LGP_TC_POLY": "0"}, {"LGP_TC_POLY": "4"},
-                                 {"LGP_TC_G": "2", "LGP_TC_DLAG": "1"}, {"LGP_TC_STAGES": "4"}])
+                                 {"LGP_TC_G": "2", "LGP_TC_DLAG": "1"}, {"LGP_TC_STAGES": "4"},
+                                 {"LGP_TC_NWG": "2"}, {"LGP_TC_D2B": "1"},
+                                 {"LGP_TC_NWG": "2", "LGP_TC_D2B": "1"}])
 def test_tensor_core_tuning_parity(gpu_ctx, monkeypatch, env):
     """K1-TC tuning knobs (exponentials on the FMA pipe per 16 entries, FP32
-    accumulation group / drain lag, TMA ring depth) meet the same bar."""
+    accumulation group / drain lag, TMA ring depth, 2 epilogue warpgroups with
+    a distance-GEMM issuer warp, one accumulator per warpgroup) meet the same
+    bar."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     expr = "(+ (scale 2.0 (rbf 0.4)) (scale 0.5 (matern32 0.9)))"
