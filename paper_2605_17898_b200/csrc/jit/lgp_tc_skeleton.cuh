@@ -84,6 +84,9 @@
 #define LGP_TC_NCI LGP_TC_NWG
 #endif
 #define TC_THREADS (32 * (1 + LGP_TC_DISTW + LGP_TC_NCI + 4 * LGP_TC_NWG))
+#if !LGP_TC_DISTW && LGP_TC_NSB > LGP_TC_STAGES
+#error "distance GEMMs queued behind the contractions need NSB <= STAGES (ring deadlock)"
+#endif
 #define TC_W_CI (1 + LGP_TC_DISTW)                 // first contraction issuer
 #define TC_W_EPI (1 + LGP_TC_DISTW + LGP_TC_NCI)   // first epilogue warp
 #if LGP_TC_N != 8 && LGP_TC_N != 16 && LGP_TC_N != 32 && LGP_TC_N != 64
