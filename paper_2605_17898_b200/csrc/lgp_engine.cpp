@@ -809,7 +809,7 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   const bool fused = op.tcsym && t == 1 && !std::getenv("LGP_CG_UNFUSED");
   // one rank: the whole vector step is one cooperative launch (cg1_vec), the
   // next direction and K1 operand included (LGP_CG_VEC3=1: the 3-launch form)
-  const bool vec1 = fused && !split && !std::getenv("LGP_CG_VEC3");
+  const bool vec1 = fused && !split && !std::getenv("LGP_CG_VEC3") && vec::cg1_vec_supported(ctx, n);
   const int64_t n_pack = std::max(op.n_rows_pad, op.n_cols_pad);
   double *part1 = nullptr, *part2 = nullptr;
   unsigned* cnt1 = nullptr;

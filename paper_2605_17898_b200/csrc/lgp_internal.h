@@ -405,6 +405,8 @@ void tcsym_epilogue_cg(Context* c, const double* rowpart, const double* colpart,
                        double scale, double noise, const double* p, double* out, double* part,
                        unsigned* counter, CgState s);
 int cg1_blocks(int64_t n);
+// the device can hold cg1_vec's whole grid at once (else the 3-kernel step)
+bool cg1_vec_supported(Context* c, int64_t n);
 // the whole single-RHS CG vector step in one cooperative launch (records ->
 // Ap, p.Ap, step, x / r update, r.r, beta / convergence, p and the K1
 // operand); bar: 2 unsigned, zeroed once

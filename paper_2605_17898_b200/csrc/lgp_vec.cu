@@ -1495,6 +1495,22 @@ void cg1_vec(Context* c, const double* rowpart, const double* colpart, const int
 
 int cg1_blocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (n + 255) / 256)); }
 
+bool cg1_vec_supported(Context* c, int64_t n) {
+  // the grid barrier needs every CTA resident at once (cooperative launch)
+  int coop = 0, per_sm = 0;
+  if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device) != cudaSuccess || !coop) {
+    cudaGetLastError();
+    return false;
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg1_vec, kVecThreads, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const int nvb = cg1_blocks(n);
+  const int grid = std::max(c->sm_count, (nvb + kVecThreads / 256 - 1) / (kVecThreads / 256));
+  return (int64_t)per_sm * c->sm_count >= grid;
+}
+
 void cg1_pap(Context* c, const double* p, const double* ap, int64_t n, double* part,
              unsigned* counter, CgState s) {
   k_cg1_pap<<<(unsigned)((n + 63) / 64), 64, 0, c->stream>>>(p, ap, n, part, counter, s);
