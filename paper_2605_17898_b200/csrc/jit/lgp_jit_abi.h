@@ -75,7 +75,7 @@ struct LgpTcArgs {
   int tiles_per_seg;
   int n_tiles;
   int seg_base;         // first column segment of this launch (staged uploads: one launch per part)
-  int pad_;
+  int seg_split;        // segments >= seg_split scale V by the second half of vscale (two parts)
   float kc[LGP_MAX_KC];
 };
 

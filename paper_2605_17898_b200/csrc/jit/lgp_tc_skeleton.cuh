@@ -739,7 +739,9 @@ extern "C" __global__ void __launch_bounds__(TC_THREADS, 1) lgp_matvec_tc(const 
       double* out = a.partial +
                     (((size_t)seg * a.n_pass + pass) * a.n_rows_pad + (size_t)rb * 128 + row) *
                         LGP_TC_N;
-      const float* sc = a.vscale + (size_t)pass * LGP_TC_N;
+      // V's power-of-two column scales are per part (column segments below /
+      // from seg_split): the staged upload packs each part as it lands
+      const float* sc = a.vscale + ((size_t)(seg >= a.seg_split ? 1 : 0) * a.n_pass + pass) * LGP_TC_N;
 #pragma unroll
       for (int i = 0; i < LGP_TC_N; i += 2) {
         const double x0 = (acc[i] + comb[((LGP_TC_NWG - 2) * LGP_TC_N + i) * 128 + row]) * (double)sc[i];

@@ -325,7 +325,7 @@ void MatvecOp::prepare() {
       c32 = (float*)ctx->scratch_get(tag + ".c32", (size_t)n_cols_pad * plan.tc_fw * 4);
     }
     vtc = ctx->scratch_get(tag + ".vtc", (size_t)n_pass * n_cols_pad * 2 * tb * 2);
-    vscale = (float*)ctx->scratch_get(tag + ".vscale", (size_t)n_pass * tb * 4);
+    vscale = (float*)ctx->scratch_get(tag + ".vscale", (size_t)2 * n_pass * tb * 4);  // [part][pass][tb]
     // inexact flag (16 B) followed by the per-column max |V| used for the scales
     v_inexact = (int*)ctx->scratch_get(tag + ".vflag", 16 + (size_t)n_pass * tb * 8);
     LgpPrepArgs pa = plan.prep;
@@ -479,6 +479,15 @@ void MatvecOp::tcsym_kernel(const int* done) {
            plan.smem_tcsym_fixed + (size_t)4096 * ts_R, &a);
 }
 
+// first column segment of V's second part (own column scales): half the
+// segments with one RHS pass and >= 2 segments, else n_seg (one part)
+int MatvecOp::tc_split() const {
+  if (n_pass != 1 || n_seg < 2) return n_seg;
+  const int s = (n_seg + 1) / 2;
+  // the second part must hold columns (trailing segments can be empty)
+  return (int64_t)s * tiles_per_seg * 64 < cols->n ? s : n_seg;
+}
+
 bool MatvecOp::run_staged(const double* V_host, double* V_dev, double* out_dev, double noise,
                           bool square, const std::function<void()>& after_copy0) {
   if (!plan.tc || tcsym || n_pass != 1 || n_seg < 2) return false;
@@ -490,12 +499,9 @@ bool MatvecOp::run_staged(const double* V_host, double* V_dev, double* out_dev, 
   // V_dev is context scratch: earlier work on the main stream may still read it
   LGP_CUDA_CHECK(cudaEventRecord(ctx->copy_ev[1], ctx->stream));
   LGP_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[1], 0));
-  // parts = runs of consecutive column segments (the K1 launch order runs
-  // segment by segment)
-  int parts = 2;
-  if (const char* e = std::getenv("LGP_STAGED_PARTS")) parts = std::max(1, atoi(e));
-  parts = std::min(parts, n_seg);
-  const int seg_per = (n_seg + parts - 1) / parts;
+  // two parts = the two runs of column segments that run() packs with their
+  // own column scales (tc_split()), so both paths give the same bits
+  const int s_split = tc_split();
   const int64_t ncols = cols->n;
   LgpTcArgs a = plan.tca;
   a.v_inexact = v_inexact;
@@ -512,11 +518,11 @@ bool MatvecOp::run_staged(const double* V_host, double* V_dev, double* out_dev, 
   a.n_pass = n_pass;
   a.tiles_per_seg = tiles_per_seg;
   a.n_tiles = n_tiles;
-  for (int h = 0; h * seg_per < n_seg; ++h) {
-    const int s0 = h * seg_per, s1 = std::min(n_seg, s0 + seg_per);
+  for (int h = 0; h < 2; ++h) {
+    const int s0 = h ? s_split : 0, s1 = h ? n_seg : s_split;
     const int64_t r0 = std::min<int64_t>((int64_t)s0 * tiles_per_seg * 64, ncols);
     const int64_t r1 = std::min<int64_t>((int64_t)s1 * tiles_per_seg * 64, ncols);
-    if (r1 <= r0 || s1 <= s0) continue;
+    if (s1 <= s0) continue;  // (tc_split: a second part always holds columns)
     LGP_CUDA_CHECK(cudaMemcpyAsync(V_dev + r0 * t, V_host + r0 * t, (size_t)(r1 - r0) * t * 8,
                                    cudaMemcpyHostToDevice, ctx->copy_stream));
     LGP_CUDA_CHECK(cudaEventRecord(ctx->copy_ev[h & 1], ctx->copy_stream));
@@ -533,9 +539,10 @@ bool MatvecOp::run_staged(const double* V_host, double* V_dev, double* out_dev, 
     // power-of-two change only shifts the FP16 exponents
     const int tile0 = s0 * tiles_per_seg;
     vec::pack_rhs_tc(ctx, V_dev + r0 * t, r1 - r0, t, (int)ceil_div<int64_t>(r1 - r0, 64), tb, 1,
-                     static_cast<char*>(vtc) + (size_t)tile0 * 2 * tb * 64 * 2, vscale, v_inexact,
-                     nullptr);
+                     static_cast<char*>(vtc) + (size_t)tile0 * 2 * tb * 64 * 2, vscale + (h ? tb : 0),
+                     v_inexact, nullptr);
     a.seg_base = s0;
+    a.seg_split = s_split;
     a.n_seg = s1 - s0;
     const int64_t grid = (int64_t)n_rb * (s1 - s0) * n_pass;
     if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
@@ -565,7 +572,19 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
                           noise, noise_v, out_dev, done);
       return;
     }
-    vec::pack_rhs_tc(ctx, V_dev, cols->n, t, n_tiles, tb, n_pass, vtc, vscale, v_inexact, done);
+    // V packed per part (column segments [0, split) and [split, n_seg)), each
+    // with its own column scales, exactly as the staged upload packs it
+    const int s_split = tc_split();
+    if (s_split < n_seg) {
+      const int64_t r_split = std::min<int64_t>((int64_t)s_split * tiles_per_seg * 64, cols->n);
+      vec::pack_rhs_tc(ctx, V_dev, r_split, t, s_split * tiles_per_seg, tb, 1, vtc, vscale, v_inexact, done);
+      vec::pack_rhs_tc(ctx, V_dev + r_split * t, cols->n - r_split, t,
+                       (int)ceil_div<int64_t>(cols->n - r_split, 64), tb, 1,
+                       static_cast<char*>(vtc) + (size_t)s_split * tiles_per_seg * 2 * tb * 64 * 2, vscale + tb,
+                       v_inexact, done);
+    } else {
+      vec::pack_rhs_tc(ctx, V_dev, cols->n, t, n_tiles, tb, n_pass, vtc, vscale, v_inexact, done);
+    }
     LgpTcArgs a = plan.tca;
     a.v_inexact = v_inexact;
     a.vscale = vscale;
@@ -583,6 +602,7 @@ void MatvecOp::run(const double* V_dev, double* out_dev, double noise, const dou
     a.tiles_per_seg = tiles_per_seg;
     a.n_tiles = n_tiles;
     a.seg_base = 0;
+    a.seg_split = s_split;
     const int64_t grid = (int64_t)n_rb * n_seg * n_pass;
     if (grid > 0x7fffffff) throw Error(LGP_E_UNSUPPORTED, "problem too large for one launch");
     prof_begin();

@@ -291,6 +291,7 @@ struct MatvecOp {
   // host-side V scan); if it throws, nothing has been launched on V yet.
   bool run_staged(const double* V_host, double* V_dev, double* out_dev, double noise, bool square,
                   const std::function<void()>& after_copy0);
+  int tc_split() const;
   // K1-TC-sym alone, on the already packed vpack (fused CG iteration)
   void tcsym_kernel(const int* done);
 };
