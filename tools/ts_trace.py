@@ -1,4 +1,5 @@
-"""Analyse a K1-TC-sym trace (LGP_TS_TRACE=<cta>): per epilogue warpgroup, the
+"""Analyse a K1-TC-sym trace (a diagnostic patch, not kept in the product kernel:
+%globaltimer stamps per chunk of warp 0 of each epilogue warpgroup): per warpgroup, the
 time its warp 0 waits for each chunk's distance GEMM (S1FULL), for the chunk's
 stage (SFULL) and works on the chunk, split by first-chunk-of-row vs others."""
 import os, sys
