@@ -517,6 +517,7 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
     op.t = t;
     op.flags = flags;
     op.allow_tc = true;
+    op.flags |= kTcAnyT;
     op.tag = "api.mv";
     op.prepare();
     // host V on one GPU through the tensor-core kernel: the upload in two

@@ -333,6 +333,10 @@ void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, doub
 std::string jit_compile(const std::string& source, std::string* log_out);
 
 // ------------------------------------------------------ AOT FP64 kernels
+// internal matvec flag (beside the public LGP_* bits): the tensor-core kernel
+// for any RHS count (the lgp_matvec API)
+constexpr uint32_t kTcAnyT = 1u << 30;
+
 namespace vec {
 // dst += src (elementwise, stream-ordered; no launch accounting: comm helper)
 void add_inplace(double* dst, const double* src, int64_t n, cudaStream_t stream);
