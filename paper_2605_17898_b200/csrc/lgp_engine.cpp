@@ -674,6 +674,18 @@ bool DonePoller::check() {
                                  ctx->stream));
   LGP_CUDA_CHECK(cudaEventRecord(ctx->done_ev[slot], ctx->stream));
   ++tail;
+  if (ctx->sharded()) {
+    // every rank must leave the loop after the same iteration (each one
+    // issues a collective): wait for this sample, whose value is the
+    // device state after this iteration - identical on every rank -
+    // instead of the first completed sample, which depends on timing
+    bool any = false;
+    for (; head < tail; ++head) {
+      LGP_CUDA_CHECK(cudaEventSynchronize(ctx->done_ev[head % 16]));
+      if (head == tail - 1) any = ctx->done_pin[head % 16] != 0;
+    }
+    return any;
+  }
   while (head < tail) {
     const int h = head % 16;
     if (tail - head > ahead) {
@@ -817,7 +829,9 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   // asynchronous copies (DonePoller): it never waits for the GPU to drain
   // (a synchronous check every 4 iterations left it idle ~30 us each time),
   // and iterations enqueued past convergence exit at their first instruction
-  int check_every = entries > 2e8 ? 2 : 8;
+  // (multi-rank: synchronous samples, so every 8 iterations - the few
+  // iterations queued past convergence are no-ops on the device)
+  int check_every = entries > 2e8 && !ctx->sharded() ? 2 : 8;
   if (const char* e = std::getenv("LGP_CG_CHECK")) check_every = std::max(1, atoi(e));
   DonePoller poll(ctx, b.s.done, entries > 2e8 ? 2 : 4);
   int done_h = 0;
@@ -1024,7 +1038,9 @@ void lanczos_device(Context* ctx, const KernelHandle* k, const Points* pts, doub
   // asynchronous copies (DonePoller): it never waits for the GPU to drain
   // (a synchronous check every 4 iterations left it idle ~30 us each time),
   // and iterations enqueued past convergence exit at their first instruction
-  int check_every = entries > 2e8 ? 2 : 8;
+  // (multi-rank: synchronous samples, so every 8 iterations - the few
+  // iterations queued past convergence are no-ops on the device)
+  int check_every = entries > 2e8 && !ctx->sharded() ? 2 : 8;
   if (const char* e = std::getenv("LGP_CG_CHECK")) check_every = std::max(1, atoi(e));
   DonePoller poll(ctx, s.done, entries > 2e8 ? 2 : 4);
   int done_h = 0;
