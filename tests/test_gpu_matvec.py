@@ -421,3 +421,25 @@ def test_staged_host_upload_matches_one_copy(gpu_ctx, monkeypatch):
     monkeypatch.setenv("LGP_NO_STAGED", "1")
     b = G.matrix_free_matvec(k, x, 0.1, v)
     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("expr", ["(rbf 0.3)", "(matern52 0.5)", "(scale 1.4 (matern32 0.4))"])
+def test_low_dimension_tensor_core(gpu_ctx, d, expr):
+    """Low-D r^2 trees take the tensor-core kernels (round 2b): the symmetric
+    CG matvec (t = 1) and the multi-RHS pass (t = 16) meet the bar, and the
+    CG matches the FP64 oracle CG's iteration count within 3 %."""
+    assert "lgp_matvec_tc(" in G.kernels.program(G.parse_kernel(expr)).source(d, 16)
+    rng = np.random.default_rng(40 + d)
+    n = 3000
+    x = rng.random((n, d))
+    nodes = O.parse_tree(expr)
+    for t in (1, 16):
+        V = rng.standard_normal((n, t)) if t > 1 else rng.standard_normal(n)
+        got = G.matrix_free_matvec(G.parse_kernel(expr), x, 0.1, V)
+        assert rel_l2(got, O.matvec(nodes, x, 0.1, V)) <= TOL
+    b = rng.standard_normal(n)
+    res = G.cg_solve(G.KernelOperator(G.parse_kernel(expr), x, 0.1), b, G.CgConfig(rel_tolerance=1e-8))
+    ref = O.cg(lambda v: O.matvec(nodes, x, 0.1, v), b, 1e-8, min(n, 1000))
+    assert abs(res.iterations - ref[1]) <= max(2, 0.03 * ref[1]), (res.iterations, ref[1])
+    assert rel_l2(res.x, ref[0]) <= 1e-4
