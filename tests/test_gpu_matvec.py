@@ -443,3 +443,22 @@ def test_low_dimension_tensor_core(gpu_ctx, d, expr):
     ref = O.cg(lambda v: O.matvec(nodes, x, 0.1, v), b, 1e-8, min(n, 1000))
     assert abs(res.iterations - ref[1]) <= max(2, 0.03 * ref[1]), (res.iterations, ref[1])
     assert rel_l2(res.x, ref[0]) <= 1e-4
+
+
+def test_staged_upload_rejects_nonfinite_v(gpu_ctx):
+    """The staged host-V path scans V while its first part is in flight: a
+    non-finite entry in either part raises NonFiniteError before any K1
+    launch reads it, and the context keeps working."""
+    rng = np.random.default_rng(19)
+    n = 50000
+    x = rng.random((n, 8))
+    v = rng.standard_normal((n, 16))
+    k = G.parse_kernel("(rbf 0.5)")
+    for row in (7, n - 3):  # first part, second part
+        bad = v.copy()
+        bad[row, 5] = np.nan
+        with pytest.raises(G.NonFiniteError):
+            G.matrix_free_matvec(k, x, 0.1, bad)
+    good = G.matrix_free_matvec(k, x, 0.1, v)
+    want = O.matvec([("rbf", (0.5,))], x, 0.1, v, block=4096, row_range=(0, 1024))
+    assert rel_l2(good[:1024], want) <= TOL
