@@ -526,7 +526,7 @@ int lgp_matvec(lgp_ctx* ctx, const lgp_kernel* k, const lgp_points* rows, const 
     if (!(flags & LGP_DEVICE_PTRS) && !ctx->sharded() && !std::getenv("LGP_NO_STAGED")) {
       double* vd = (double*)ctx->scratch_get("api.V", (size_t)cols->n * t * 8);
       staged = op.run_staged(V, vd, od, square ? noise : 0.0, square, [&]() {
-        if (scan_v) check_finite(V, (size_t)cols->n * t, "V");  // while part 0 is in flight
+        if (scan_v) check_finite(V, (size_t)cols->n * t, "V");  // while part 0's K1 runs
       });
     }
     if (!staged) {

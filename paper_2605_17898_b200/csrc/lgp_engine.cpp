@@ -526,11 +526,16 @@ bool MatvecOp::run_staged(const double* V_host, double* V_dev, double* out_dev, 
     LGP_CUDA_CHECK(cudaMemcpyAsync(V_dev + r0 * t, V_host + r0 * t, (size_t)(r1 - r0) * t * 8,
                                    cudaMemcpyHostToDevice, ctx->copy_stream));
     LGP_CUDA_CHECK(cudaEventRecord(ctx->copy_ev[h & 1], ctx->copy_stream));
-    if (h == 0 && after_copy0) {
+    // the host-side V scan once every copy is queued, while the first part's
+    // K1 runs (a pageable copy blocks the host, so scanning right after the
+    // first copy would delay that K1); on failure nothing is returned and
+    // the streams drain first (the caller may free V right away)
+    if ((h == 1 || s_split >= n_seg) && after_copy0) {
       try {
         after_copy0();
       } catch (...) {
-        cudaStreamSynchronize(ctx->copy_stream);  // the caller may free V right away
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamSynchronize(ctx->stream);
         throw;
       }
     }

@@ -287,8 +287,9 @@ struct MatvecOp {
   // on the copy stream, each part's pack + K1 launch (its column segments)
   // queued as soon as the part has landed, so the second part's transfer
   // overlaps the first part's K1. True if it ran (else the caller stages V).
-  // after_copy0 runs on the host once the first part's copy is queued (the
-  // host-side V scan); if it throws, nothing has been launched on V yet.
+  // after_copy0 runs on the host once every part's copy is queued, while the
+  // first part's K1 runs (the host-side V scan); if it throws, the streams
+  // are drained and the exception propagates (no result is returned).
   bool run_staged(const double* V_host, double* V_dev, double* out_dev, double noise, bool square,
                   const std::function<void()>& after_copy0);
   int tc_split() const;
