@@ -849,6 +849,9 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
   // one rank: the whole vector step is one cooperative launch (cg1_vec), the
   // next direction and K1 operand included (LGP_CG_VEC3=1: the 3-launch form)
   const bool vec1 = fused && !split && !std::getenv("LGP_CG_VEC3") && vec::cg1_vec_supported(ctx, n);
+  // multi-rank: after the all-reduce of Ap, the same one-launch step from Ap
+  // (p.Ap shares as k_cg1_pap's, then update, beta and the next direction)
+  const bool vec1s = fused && split && !std::getenv("LGP_CG_VEC3") && vec::cg1_vec_supported(ctx, n);
   const int64_t n_pack = std::max(op.n_rows_pad, op.n_cols_pad);
   double *part1 = nullptr, *part2 = nullptr;
   unsigned* cnt1 = nullptr;
@@ -859,7 +862,7 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
     part2 = part1 + np;
     cnt1 = reinterpret_cast<unsigned*>(part1 + 2 * np);
     LGP_CUDA_CHECK(cudaMemsetAsync(cnt1, 0, ncnt * 4, ctx->stream));
-    if (vec1) vec::cg1_pack(ctx, b.p, b.r, op.vpack, n, n_pack, b.s);  // beta = 0: p = r = b
+    if (vec1 || vec1s) vec::cg1_pack(ctx, b.p, b.r, op.vpack, n, n_pack, b.s);  // beta = 0: p = r = b
   }
   unsigned long long* vtrace = nullptr;
   if (vec1 && std::getenv("LGP_CG_VEC_TRACE")) {
@@ -889,6 +892,19 @@ void cg_device(Context* ctx, const KernelHandle* k, const Points* pts, double no
                        (mx - tr[0]) * 1e-3);
         }
       }
+      if (nsh > 0) vec::cg_shift(ctx, xs, ps, b.r, n, nsh, sig, sst, b.s, it);
+    } else if (vec1s) {
+      {
+        auto ev = k1_event_begin(ctx);
+        op.tcsym_kernel(b.s.done);
+        k1_event_end(ctx, ev);
+      }
+      vec::tcsym_epilogue(ctx, op.partial, op.colpart, op.r_ptr, op.r_rec, op.c_ptr, op.c_rec, n,
+                          op.plan.root_scale, ctx->rank == 0 ? noise : 0.0,
+                          ctx->rank == 0 ? b.p : nullptr, b.ap, b.s.done);
+      comm_allreduce_sum_inplace(ctx->comm, b.ap, (size_t)n, ctx->stream);
+      vec::cg1_vec(ctx, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, n, n_pack, 1.0, 0.0, b.x,
+                   b.r, b.p, b.ap, op.vpack, part1, part2, cnt1, it, max_iter, b.s, vtrace);
       if (nsh > 0) vec::cg_shift(ctx, xs, ps, b.r, n, nsh, sig, sst, b.s, it);
     } else if (fused) {
       vec::cg1_pack(ctx, b.p, b.r, op.vpack, n, n_pack, b.s);

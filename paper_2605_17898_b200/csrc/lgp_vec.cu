@@ -693,14 +693,15 @@ __global__ void __launch_bounds__(kVecThreads, 1)
         e = make_int4(__ldg(c_ptr + c), __ldg(c_ptr + c + 1), __ldg(r_ptr + I), __ldg(r_ptr + I + 1));
       }
     };
+    const bool recs = rowpart != nullptr;  // else Ap is given (multi-rank: all-reduced)
     int4 eb = make_int4(0, 0, 0, 0), en = eb;
-    bounds((long long)kVecQB * blockIdx.x + qb, eb);
+    if (recs) bounds((long long)kVecQB * blockIdx.x + qb, eb);
     for (long long c0 = (long long)kVecQB * blockIdx.x; c0 < nc; c0 += (long long)kVecQB * gridDim.x) {
       const long long c = c0 + qb;
-      bounds(c + (long long)kVecQB * gridDim.x, en);
+      if (recs) bounds(c + (long long)kVecQB * gridDim.x, en);
       // this block's p entries, loaded alongside the records
       const double pi = (lt < 64 && c < nc && c * 64 + lt < n) ? p[c * 64 + lt] : 0.0;
-      if (c < nc) {
+      if (recs && c < nc) {
         const int rr = (int)(c & 1) * 64 + j2;
         const double2 cs = sum_records2<64>(colpart, c_rec, eb.x, eb.y, g, j2);
         const double2 rs = sum_records2<128>(rowpart, r_rec, eb.z, eb.w, g, rr);
@@ -715,15 +716,19 @@ __global__ void __launch_bounds__(kVecThreads, 1)
         const long long i = c * 64 + jj;
         double d = 0.0;
         if (c < nc && i < n) {
-          double o = 0.0;
+          if (recs) {
+            double o = 0.0;
 #pragma unroll
-          for (int u = 0; u < kTsGroups; ++u) o += pt[qb][0][u][jj];
+            for (int u = 0; u < kTsGroups; ++u) o += pt[qb][0][u][jj];
 #pragma unroll
-          for (int u = 0; u < kTsGroups; ++u) o += pt[qb][1][u][jj];
-          o = __dmul_rn(scale, o);
-          if (noise != 0.0) o = __dadd_rn(o, __dmul_rn(noise, pi));
-          ap[i] = o;
-          d = pi * o;
+            for (int u = 0; u < kTsGroups; ++u) o += pt[qb][1][u][jj];
+            o = __dmul_rn(scale, o);
+            if (noise != 0.0) o = __dadd_rn(o, __dmul_rn(noise, pi));
+            ap[i] = o;
+            d = pi * o;
+          } else {
+            d = pi * ap[i];  // k_cg1_pap's share
+          }
         }
         // block_sum_fixed of the 64-thread block: each warp's xor tree, then
         // the two warps in order
