@@ -614,7 +614,9 @@ __global__ void __launch_bounds__(256) k_cg1_update(double* __restrict__ x, doub
 // 64-lane order as sum_shares), so no CTA waits for a "last block", and the
 // arithmetic is the 3-kernel sequence's bit for bit: the p.Ap shares are
 // per 64-row block (k_tcsym_epilogue_cg / k_cg1_pap), the r.r shares per
-// virtual 256-thread block of k_cg1_update's grid-stride layout.
+// virtual 256-thread block of k_cg1_update's grid-stride layout. With
+// rowpart == nullptr the records phase is skipped and Ap is read as given
+// (the multi-rank CG, after its all-reduce).
 constexpr int kVecThreads = 1024;
 constexpr int kVecQB = kVecThreads / 256;  // 64-row blocks per record round
 
