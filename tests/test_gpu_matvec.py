@@ -346,7 +346,8 @@ def test_results_in_pinned_buffers_survive(gpu_ctx):
 @pytest.mark.parametrize("env", [{"LGP_TC_POLY": "0"}, {"LGP_TC_POLY": "4"},
                                  {"LGP_TC_G": "2", "LGP_TC_DLAG": "1"}, {"LGP_TC_STAGES": "4"},
                                  {"LGP_TC_NWG": "2"}, {"LGP_TC_D2B": "1"},
-                                 {"LGP_TC_NWG": "2", "LGP_TC_D2B": "1"}])
+                                 {"LGP_TC_NWG": "2", "LGP_TC_D2B": "1"}, {"LGP_TC_NCI": "2"},
+                                 {"LGP_TC_NSB": "3"}])
 def test_tensor_core_tuning_parity(gpu_ctx, monkeypatch, env):
     """K1-TC tuning knobs (exponentials on the FMA pipe per 16 entries, FP32
     accumulation group / drain lag, TMA ring depth, 2 epilogue warpgroups with
